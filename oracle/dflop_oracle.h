@@ -1,0 +1,148 @@
+/*
+ * dflop_oracle.h -- ORACLE header.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU reference for the DFLOP plan-candidate path
+ * (arXiv 2603.25120, "DFLOP: A Data-driven Framework for Multimodal LLM Training
+ * Pipeline Optimization").  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load it.  The product path
+ * (paper_2603_25120_b200/, include/dflop.h) never includes, links or executes
+ * anything under oracle/, and this header shares nothing with include/dflop.h.
+ *
+ * Citations: "P:n" = PAPER.md line n; "S:n" = SPEC.md line n; "R<k>" = the
+ * reading number k in DESIGN.md section 3 (the ambiguity register).
+ */
+#ifndef DFLOP_ORACLE_H
+#define DFLOP_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_MAX_X 32
+#define ORC_MAX_TP 4
+
+/* Throughput grid X(x, tp) in FLOP/s per GPU, measured at knots. */
+typedef struct orc_grid {
+    uint32_t n_x;                       /* 1..32 shape knots   */
+    uint32_t n_tp;                      /* 1..4  TP knots      */
+    double x[ORC_MAX_X];                /* strictly increasing */
+    double tp[ORC_MAX_TP];              /* strictly increasing */
+    double v[ORC_MAX_TP][ORC_MAX_X];    /* v[a][k] at (x_k, tp_a) */
+} orc_grid;
+
+/* Memory grid M(l, tp, x) in bytes: two layer counts, TP knots, shape knots. */
+typedef struct orc_mgrid {
+    uint32_t n_x;
+    uint32_t n_tp;
+    double l[2];
+    double tp[ORC_MAX_TP];
+    double x[ORC_MAX_X];
+    double v[2][ORC_MAX_TP][ORC_MAX_X];
+} orc_mgrid;
+
+/* MLLM cost model: encoder + LLM shapes (Table 1) and profiled grids. */
+typedef struct orc_model {
+    uint32_t e_layers;   /* E_l                                    */
+    uint32_t e_hidden;   /* h_E                                    */
+    uint32_t e_seq;      /* E_seq_len: tokens per encoder instance */
+    uint32_t e_attn;     /* 1: add in-tile attention 4*h_E*E_seq^2 */
+    uint32_t l_layers;   /* L_l                                    */
+    uint32_t l_hidden;   /* h_L                                    */
+    uint32_t tau_tile;   /* LLM tokens per image tile              */
+    uint32_t tau_frame;  /* LLM tokens per video frame             */
+    double bwd_ratio;    /* backward / forward (2.0)        */
+    double tick_ns;      /* integer time unit in ns (R19)          */
+    orc_grid thr_e;      /* E_thr(b, E_tp)                         */
+    orc_grid thr_att;    /* L_attn_thr(s, L_tp)                    */
+    orc_grid thr_lin;    /* L_lin_thr(s, L_tp)                     */
+} orc_model;
+
+typedef struct orc_mem {
+    orc_mgrid ms_e;      /* model_state_E(l, E_tp)        */
+    orc_mgrid as_e;      /* act_state_E(l, E_tp, b)       */
+    orc_mgrid ms_l;      /* model_state_L(l, L_tp)        */
+    orc_mgrid as_l;      /* act_state_L(l, L_tp, s)       */
+    double mem_per_gpu;  /* M_gpu, bytes                  */
+} orc_mem;
+
+/* theta = (E_tp, E_pp, E_dp, L_tp, L_pp, L_dp, N_mb). */
+typedef struct orc_plan {
+    uint32_t e_tp, e_pp, e_dp, l_tp, l_pp, l_dp, n_mb;
+} orc_plan;
+
+typedef struct orc_bparams {
+    uint32_t mode;       /* 0 = heuristic candidate family, 1 = exhaustive */
+    uint32_t K;          /* family size                                   */
+    uint32_t R;          /* refinement rounds                             */
+    uint32_t G;          /* perturbation group size 1..16                 */
+    uint32_t seed[2];    /* Philox key                                    */
+} orc_bparams;
+
+/* Status codes (mirrors the meaning, not the header, of the product ABI). */
+#define ORC_OK 0
+#define ORC_INVALID 1
+#define ORC_OVERFLOW 3
+#define ORC_INFEASIBLE 4
+
+/* Philox4x32-10 (Salmon et al., SC'11), from its specification. */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+uint32_t orc_mulhi32(uint32_t u, uint32_t n);
+
+/* Linear interpolation, R3: clamped multilinear, (1-w)a + w b form. */
+double orc_interp_thr(const orc_grid* g, double x, double tp);
+double orc_interp_mem(const orc_mgrid* g, double l, double tp, double x);
+
+/* Step a1: per-item stage costs (O1-O4).  cost_f64[4][n] in ns (ef, eb, lf, lb),
+ * cost_q[4][n] in ticks.  Returns ORC_OVERFLOW (and the first index in *bad) when a cost
+ * rounds to >= 2^32 ticks. */
+int orc_predict(const orc_model* m, const orc_plan* p, const uint32_t* tiles, const uint32_t* frames,
+                const uint32_t* text, uint32_t n, double* cost_f64, uint32_t* cost_q, uint32_t* bad);
+
+/* Step a2: base order pi: key max(e_i, l_i) descending, index ascending. */
+void orc_base_order(const uint32_t* cost_q, uint32_t n, uint32_t* order);
+
+/* Step a4 building block: non-interleaved 1F1B over S stages x M microbatches,
+ * worklist evaluation.  fwd/bwd are [S][M] row-major.  stage_busy[S] may be NULL. */
+int orc_simulate_1f1b(const uint64_t* fwd, const uint64_t* bwd, uint32_t S, uint32_t M,
+                      uint64_t* makespan, uint64_t* stage_busy);
+
+/* Steps a3+a4 for one candidate c.  assign[n] (may be NULL) receives the bucket of item i. */
+int orc_run_candidate(const uint32_t* cost_q, uint32_t n, const orc_plan* p, const orc_bparams* bp,
+                      const uint32_t* order, uint32_t c, uint32_t* assign, uint64_t* T, uint64_t* cmax);
+
+/* Steps a2..a5 over candidates [c0, c1).  cand_T / cand_cmax (may be NULL) get per-candidate
+ * scores; the lexicographic minimum of (T, c) is returned with its assignment. */
+int orc_balance(const uint32_t* cost_q, uint32_t n, const orc_plan* p, const orc_bparams* bp,
+                uint32_t c0, uint32_t c1, uint64_t* cand_T, uint64_t* cand_cmax,
+                uint64_t* best_T, uint32_t* best_c, uint64_t* best_cmax, uint32_t* best_assign);
+
+/* CSR index groups ("returns a set of index groups"): bucket-major, items ascending. */
+void orc_groups(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items);
+
+/* Algorithm 1 phase 1. */
+uint32_t orc_find_combs(uint32_t gpus, uint32_t gpus_per_node, uint32_t* out3, uint32_t cap);
+uint64_t orc_enumerate_configs(uint32_t n_gpus, uint32_t gpus_per_node, uint32_t* out6, uint64_t cap);
+
+/* Batch means b-bar, s-bar, integer sums divided by n. */
+void orc_batch_means(const orc_model* m, const uint32_t* tiles, const uint32_t* frames,
+                     const uint32_t* text, uint32_t n, double* mean_b, double* mean_s);
+
+/* Algorithm 1 phase 2 for one (config, i) pair: returns 1 if feasible and writes T_A. */
+int orc_stage_a_pair(const orc_model* m, const orc_mem* mm, const uint32_t cfg6[6], uint32_t i,
+                     uint32_t gbs, double mean_b, double mean_s, uint64_t* T_A,
+                     double* mem_e, double* mem_l, uint64_t* e_dur, uint64_t* l_dur);
+
+/* Stage A over every config and i = 1..GBS//L_dp, in enumeration order.  T_A[pair] is
+ * UINT64_MAX when infeasible.  Returns the number of pairs written (<= cap). */
+uint64_t orc_stage_a_all(const orc_model* m, const orc_mem* mm, uint32_t n_gpus, uint32_t gpus_per_node,
+                         uint32_t gbs, double mean_b, double mean_s, uint64_t* T_A, uint64_t cap);
+
+/* Top-P feasible pairs by (T_A, eps, i): writes pair indices (enumeration order) into top[]. */
+uint32_t orc_stage_a_top(const uint64_t* T_A, uint64_t n_pairs, uint32_t P, uint64_t* top);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,486 @@
+"""Pins for the CPU oracle (oracle/dflop_oracle.c) against things other than itself:
+Random123 KAT, SPEC worked examples (tests/golden/), closed forms, invariants,
+brute force and an explicit-DAG longest path (tests/bruteforce.py).  -m "not gpu".
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import bruteforce as BF
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ helpers
+def const_grid(v, tp=(1.0, 2.0, 4.0, 8.0), x=(1.0, 2.0)):
+    return dict(x=list(x), tp=list(tp), v=[[float(v)] * len(x) for _ in tp])
+
+
+def unit_model(thr_e=1e9, thr_att=1e9, thr_lin=1e9, tau_tile=0, tau_frame=0, tick_ns=1.0, r=2.0, e_attn=0):
+    return dict(e_layers=1, e_hidden=1, e_seq=1, e_attn=e_attn, l_layers=1, l_hidden=1, tau_tile=tau_tile,
+                tau_frame=tau_frame, bwd_ratio=r, tick_ns=tick_ns, thr_e=const_grid(thr_e),
+                thr_att=const_grid(thr_att), thr_lin=const_grid(thr_lin))
+
+
+def plan(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=1, l_dp=1, n_mb=1):
+    return dict(e_tp=e_tp, e_pp=e_pp, e_dp=e_dp, l_tp=l_tp, l_pp=l_pp, l_dp=l_dp, n_mb=n_mb)
+
+
+def loads_1d(loads):
+    """cost matrix with e_i = load (ef = load, eb = 0) and l_i = 0: one-dimensional loads."""
+    n = len(loads)
+    c = np.zeros((4, n), np.uint32)
+    c[0] = loads
+    return c
+
+
+def spec(name):
+    rows = []
+    for line in open(os.path.join(GOLD, "spec_examples.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        parts = [p.strip() for p in line.split("|")]
+        if parts[0] == name:
+            rows.append(parts)
+    assert rows, name
+    return rows
+
+
+def kv(s):
+    out = {}
+    for tok in s.split():
+        k, v = tok.split("=")
+        out[k] = v
+    return out
+
+
+# ------------------------------------------------------------------ Philox
+def test_philox_kat(O):
+    n = 0
+    for line in open(os.path.join(GOLD, "philox_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        w = [int(t, 16) for t in line.split()]
+        assert list(O.philox(w[0:4], w[4:6])) == w[6:10]
+        n += 1
+    assert n == 3
+
+
+def test_mulhi32_range(O):
+    assert O.mulhi32(0, 7) == 0
+    assert O.mulhi32(0xFFFFFFFF, 7) == 6
+    assert O.mulhi32(0x80000000, 10) == 5
+
+
+# ------------------------------------------------------------------ interpolation
+def test_interp_spec_examples(O):
+    g = dict(x=[1.0, 2.0], tp=[1.0], v=[[10.0, 20.0]])
+    assert O.interp_thr(g, 1.5, 1.0) == 15.0
+    assert O.interp_thr(g, 2.0, 1.0) == 20.0
+    assert O.interp_thr(g, 5.0, 1.0) == 20.0   # clamp
+    assert O.interp_thr(g, 0.0, 1.0) == 10.0
+
+
+def test_interp_exact_at_knots(O, presets):
+    g = presets[5].model["thr_att"]
+    for a, t in enumerate(g["tp"]):
+        for k, x in enumerate(g["x"]):
+            assert O.interp_thr(g, x, t) == g["v"][a][k]   # zero tolerance
+
+
+def test_interp_bilinear_closed_form(O):
+    xs, ts = [1.0, 3.0, 4.0, 10.0], [1.0, 2.0, 4.0, 8.0]
+    f = lambda x, y: 3 * x + 2 * y + x * y
+    g = dict(x=xs, tp=ts, v=[[f(x, t) for x in xs] for t in ts])
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        x, t = rng.uniform(1, 10), rng.uniform(1, 8)
+        assert abs(O.interp_thr(g, x, t) - f(x, t)) <= 1e-12 * f(x, t)
+
+
+def test_interp_monotone(O, presets):
+    g = presets[1].model["thr_lin"]
+    xs = np.linspace(1, 200000, 3001)
+    v = [O.interp_thr(g, float(x), 4.0) for x in xs]
+    assert all(b >= a * (1 - 1e-15) for a, b in zip(v, v[1:]))   # S:160 (up to one rounding)
+
+
+def test_mem_interp_linear_formula(O, presets):
+    from paper_2603_25120_b200 import synth
+    mem = presets[4].mem()
+    he, es = presets[4].model["e_hidden"], presets[4].model["e_seq"]
+    for l in (1, 3, 7, 45):
+        for tp in (1, 2, 4, 8):
+            for b in (0.0, 1.0, 37.5, 1000.0):
+                exact = 34.0 * l * b * es * he / tp
+                assert abs(O.interp_mem(mem["as_e"], l, tp, b) - exact) <= 1e-9 * max(exact, 1.0)
+            ms = 16.0 * 12.0 * he * he * l / tp
+            assert abs(O.interp_mem(mem["ms_e"], l, tp, 0.0) - ms) <= 1e-9 * ms
+
+
+# ------------------------------------------------------------------ predict (step a1)
+def test_item_flops_unit_values(O):
+    # unit spec, b=1, s=1 -> e=24, lin=24, attn=4.  Throughput 1e9 FLOP/s -> 1 ns per FLOP.
+    t, f, x = [1], [0], [1]
+    cf, q, st, _ = O.predict(unit_model(thr_att=1e30), plan(), t, f, x)
+    assert st == 0 and cf[0, 0] == 24.0
+    assert abs(cf[2, 0] - 24.0) < 1e-12                      # linear only
+    cf, q, st, _ = O.predict(unit_model(thr_lin=1e30), plan(), t, f, x)
+    assert abs(cf[2, 0] - 4.0) < 1e-12                       # attention only
+    cf, q, st, _ = O.predict(unit_model(), plan(), t, f, x)
+    assert cf[2, 0] == 28.0 and list(q[:, 0]) == [24, 48, 28, 56]   # backward = 2x
+
+
+def test_predict_zero_encoder_batch(O, presets):
+    p = presets[2]
+    cf, q, st, _ = O.predict(p.model, p.plan, [0, 0], [0, 0], [100, 5000])
+    assert st == 0 and (cf[0] == 0).all() and (cf[1] == 0).all() and (q[:2] == 0).all()
+
+
+def test_predict_homogeneity_and_packing(O):
+    m = unit_model(thr_att=1e9, thr_lin=1e30)
+    cf, _, _, _ = O.predict(m, plan(), [1, 3, 7], [0, 0, 0], [1, 2, 4])
+    assert cf[0, 1] == 3 * cf[0, 0] and cf[0, 2] == 7 * cf[0, 0]          # S:242 homogeneous
+    assert abs(cf[2, 1] - 4 * cf[2, 0]) < 1e-9 and abs(cf[2, 2] - 16 * cf[2, 0]) < 1e-9   # s^2 attention
+    m = unit_model(thr_att=1e30, thr_lin=1e9)
+    cf, _, _, _ = O.predict(m, plan(), [0, 0], [0, 0], [5, 10])
+    assert abs(cf[2, 1] - 2 * cf[2, 0]) < 1e-9                              # linear in s
+
+
+def test_predict_parallel_degrees(O):
+    m = unit_model()
+    base, _, _, _ = O.predict(m, plan(), [4], [0], [8])
+    p = plan(e_tp=2, e_pp=2, l_tp=4, l_pp=2)
+    cf, _, _, _ = O.predict(m, p, [4], [0], [8])
+    assert abs(cf[0, 0] - base[0, 0] / 4) < 1e-9       # / (E_tp * E_pp) at constant thr
+    assert abs(cf[2, 0] - base[2, 0] / 8) < 1e-9       # / (L_tp * L_pp)
+    cf, _, _, _ = O.predict(m, plan(e_dp=2, l_dp=4), [4], [0], [8])
+    assert abs(cf[0, 0] - base[0, 0] * 2) < 1e-9       # R13: x L_dp / E_dp
+
+
+def test_predict_tokens_and_frames(O):
+    m = unit_model(thr_att=1e30, tau_tile=10, tau_frame=3)
+    cf, _, _, _ = O.predict(m, plan(), [2, 0], [0, 5], [1, 1])
+    # b = tiles + frames; s = text + 10*tiles + 3*frames
+    assert cf[0, 0] == 2 * 24.0 and cf[0, 1] == 5 * 24.0
+    assert abs(cf[2, 0] - 24.0 * 21) < 1e-9 and abs(cf[2, 1] - 24.0 * 16) < 1e-9
+
+
+def test_predict_rounding_and_overflow(O):
+    m = unit_model(thr_lin=1e30, thr_att=1e30, tick_ns=48.0)     # e = 24 ns -> 0.5 tick -> 0 (half even)
+    _, q, st, _ = O.predict(m, plan(), [1, 3], [0, 0], [1, 1])
+    assert st == 0 and q[0, 0] == 0 and q[1, 0] == 1 and q[0, 1] == 2   # 0.5->0, 1.0->1, 1.5->2
+    m = unit_model(thr_e=1e-3)                                     # 24 FLOP at 1e-3 FLOP/s -> 2.4e13 ns
+    _, q, st, bad = O.predict(m, plan(), [0, 1], [0, 0], [1, 1])
+    assert st == 3 and bad == 1
+
+
+# ------------------------------------------------------------------ order (a2)
+def test_base_order(O):
+    c = loads_1d([5, 9, 9, 1, 7, 9])
+    c[2, 3] = 50                      # item 3: l = 50 + 0 dominates
+    assert list(O.base_order(c)) == [3, 1, 2, 5, 4, 0]
+
+
+# ------------------------------------------------------------------ 1F1B (a4)
+def test_1f1b_uniform_closed_form(O):
+    for S in range(1, 9):
+        for M in range(1, 20):
+            for f, b in ((1, 2), (3, 5), (2, 1), (1, 1)):
+                F = np.full((S, M), f)
+                B = np.full((S, M), b)
+                T, busy = O.simulate_1f1b(F, B)
+                assert T == (M + S - 1) * (f + b)                    # P:477 with max(E,L)=f+b
+                assert (busy == M * (f + b)).all()
+
+
+def test_1f1b_single_stage(O):
+    T, _ = O.simulate_1f1b([[3, 1, 4]], [[1, 5, 9]])
+    assert T == 3 + 1 + 4 + 1 + 5 + 9
+
+
+def test_1f1b_ideal_bubble(O):
+    # idle fraction (p-1)/m
+    for S in range(1, 7):
+        for M in range(1, 33):
+            T, busy = O.simulate_1f1b(np.full((S, M), 2), np.full((S, M), 4))
+            idle = (S * T - int(busy.sum())) / int(busy.sum())
+            assert abs(idle - (S - 1) / M) <= 1e-9 * max(1.0, (S - 1) / M)
+    for p, m, want in ((4, 6, 0.5), (4, 12, 0.25), (1, 7, 0.0)):
+        T, busy = O.simulate_1f1b(np.full((p, m), 1), np.full((p, m), 2))
+        assert abs((p * T - busy.sum()) / busy.sum() - want) < 1e-12
+
+
+def test_1f1b_matches_explicit_dag(O):
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        S, M = int(rng.integers(1, 7)), int(rng.integers(1, 9))
+        F = rng.integers(0, 20, (S, M))
+        B = rng.integers(0, 40, (S, M))
+        T, _ = O.simulate_1f1b(F, B)
+        assert T == BF.dag_makespan(F.tolist(), B.tolist())
+
+
+def test_1f1b_sandwich_and_monotone(O):
+    rng = np.random.default_rng(8)
+    for _ in range(500):
+        S, M = int(rng.integers(1, 6)), int(rng.integers(1, 8))
+        F = rng.integers(0, 50, (S, M))
+        B = rng.integers(0, 100, (S, M))
+        T, _ = O.simulate_1f1b(F, B)
+        lo = int((F + B).sum(axis=1).max())
+        hi = (M + S - 1) * int((F + B).max())
+        assert lo <= T <= hi                                            # R23 / SURVEY 4 item 2
+        s, k = int(rng.integers(S)), int(rng.integers(M))
+        F2 = F.copy()
+        F2[s, k] += int(rng.integers(1, 10))
+        assert O.simulate_1f1b(F2, B)[0] >= T                           # fixed DAG => monotone
+
+
+def test_1f1b_counterexample_from_survey(O):
+    # S=2, M=1, F=(1,10), B=(2,20): simulation 33 < formula 60
+    T, _ = O.simulate_1f1b([[1], [10]], [[2], [20]])
+    assert T == 33
+
+
+# ------------------------------------------------------------------ LPT / candidates (a3)
+def test_lpt_spec_example(O):
+    rows = spec("lpt")
+    c = loads_1d([5, 4, 3, 3, 2, 1])
+    a, T, cm = O.run_candidate(c, plan(n_mb=3), K=2, R=0, G=1, seed=(0, 0), c=0)
+    groups = sorted(sorted(int(c[0, i]) for i in range(6) if a[i] == j) for j in range(3))
+    assert groups == [[1, 5], [2, 4], [3, 3]] and cm == 6
+
+
+def test_lpt_graham_tight(O):
+    c = loads_1d([3, 3, 2, 2, 2])
+    _, _, cm = O.run_candidate(c, plan(n_mb=2), K=2, R=0, G=1, seed=(0, 0), c=0)
+    assert cm == 7 and BF.opt_cmax_1d([3, 3, 2, 2, 2], 2) == 6         # 7/6 = 4/3 - 1/6
+    assert BF.opt_cmax_1d([8, 7, 6, 5, 4], 2) == 15
+
+
+def test_lpt_graham_bound_and_rules_coincide_1d(O):
+    rng = np.random.default_rng(3)
+    for _ in range(150):
+        n, m = int(rng.integers(1, 9)), int(rng.integers(1, 4))
+        loads = rng.integers(1, 30, n).tolist()
+        c = loads_1d(loads)
+        a0, _, cm0 = O.run_candidate(c, plan(n_mb=m), K=2, R=0, G=1, seed=(0, 0), c=0)
+        a1, _, cm1 = O.run_candidate(c, plan(n_mb=m), K=2, R=0, G=1, seed=(0, 0), c=1)
+        assert list(a0) == list(a1)                                     # one dimension: rules coincide
+        opt = BF.opt_cmax_1d(loads, m)
+        assert cm0 * 3 * m <= (4 * m - 1) * opt                         # Graham: 4/3 - 1/(3m)
+        assert cm0 == BF.lpt_1d(loads, m)[1]
+
+
+def test_candidate_partition_and_lower_bound(O, presets):
+    p = presets[2]
+    t, f, x = p.features(0)
+    _, q, _, _ = O.predict(p.model, p.plan, t, f, x)
+    m = p.plan["n_mb"] * p.plan["l_dp"]
+    e = q[0].astype(np.int64) + q[1]
+    l = q[2].astype(np.int64) + q[3]
+    lb = max(-(-int(e.sum()) // m), -(-int(l.sum()) // m), int(np.maximum(e, l).max()))
+    for c in (0, 1, 2, 17, 999):
+        a, T, cm = O.run_candidate(q, p.plan, K=p.K, R=p.R, G=p.G, seed=p.seed(0), c=c)
+        assert len(a) == p.n and a.max() < m                            # each item exactly once
+        sums_e = np.bincount(a, weights=e, minlength=m)
+        sums_l = np.bincount(a, weights=l, minlength=m)
+        assert cm == int(max(sums_e.max(), sums_l.max()))               # C_max recomputed
+        assert cm >= lb
+        assert T >= cm                                                  # a bucket's stage time is inside T
+
+
+def test_refinement_never_increases_cmax(O, presets):
+    p = presets[3]
+    t, f, x = p.features(1)
+    _, q, _, _ = O.predict(p.model, p.plan, t, f, x)
+    for c in (2, 3, 40):
+        prev = None
+        for R in range(0, 12):
+            _, _, cm = O.run_candidate(q, p.plan, K=p.K, R=R, G=p.G, seed=p.seed(1), c=c)
+            if prev is not None:
+                assert cm <= prev
+            prev = cm
+
+
+def test_perturbation_is_group_local(O, presets):
+    # c >= 2 with R = 0 and G = 1 has no freedom: identical to c = 1
+    p = presets[2]
+    t, f, x = p.features(0)
+    _, q, _, _ = O.predict(p.model, p.plan, t, f, x)
+    a1, T1, _ = O.run_candidate(q, p.plan, K=8, R=0, G=1, seed=(1, 2), c=1)
+    a5, T5, _ = O.run_candidate(q, p.plan, K=8, R=0, G=1, seed=(1, 2), c=5)
+    assert list(a1) == list(a5) and T1 == T5
+
+
+def test_exhaustive_matches_bruteforce(O):
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        n = int(rng.integers(1, 7))
+        pl = plan(e_pp=int(rng.integers(1, 3)), l_pp=int(rng.integers(1, 3)), n_mb=int(rng.integers(1, 3)),
+                  l_dp=int(rng.integers(1, 3)))
+        m = pl["n_mb"] * pl["l_dp"]
+        if m ** n > 5000:
+            continue
+        cost = rng.integers(0, 30, (4, n)).astype(np.uint32)
+        K = m ** n
+        r = O.balance(cost, pl, K=K, R=0, G=1, seed=(0, 0), mode=1)
+        bf = list(BF.all_assignments(cost.tolist(), pl))
+        Tmin = min(b[2] for b in bf)
+        cstar = min(b[0] for b in bf if b[2] == Tmin)
+        assert r["T"] == Tmin and r["c"] == cstar
+        for idx, a, T, cm in bf:
+            assert r["cand_T"][idx] == T and r["cand_cmax"][idx] == cm
+
+
+def test_best_of_k_vs_bruteforce_cmax(O):
+    rng = np.random.default_rng(12)
+    hits = 0
+    for trial in range(15):
+        n = int(rng.integers(4, 9))
+        pl = plan(n_mb=int(rng.integers(2, 4)), l_pp=1)
+        cost = rng.integers(1, 40, (4, n)).astype(np.uint32)
+        r = O.balance(cost, pl, K=32, R=8, G=4, seed=(trial, 9))
+        best_c = int(r["cand_cmax"].min())
+        opt = min(b[3] for b in BF.all_assignments(cost.tolist(), pl))
+        assert best_c >= opt
+        hits += best_c == opt
+    assert hits >= 5   # reported, not a proof
+
+
+def test_groups_csr(O):
+    a = np.array([2, 0, 2, 1, 0, 2], np.uint32)
+    off, items = O.groups(a, 4)
+    assert list(off) == [0, 2, 3, 6, 6]
+    assert list(items) == [1, 4, 3, 0, 2, 5]
+
+
+def test_quality_within_one_percent_of_lb(O, presets):
+    # "load imbalance deviates by less than 1% from the theoretical lower bound"
+    p = presets[5]
+    t, f, x = p.features(0)
+    _, q, _, _ = O.predict(p.model, p.plan, t, f, x)
+    m = p.plan["n_mb"] * p.plan["l_dp"]
+    e = q[0].astype(np.int64) + q[1]
+    l = q[2].astype(np.int64) + q[3]
+    lb = max(-(-int(e.sum()) // m), -(-int(l.sum()) // m), int(np.maximum(e, l).max()))
+    r = O.balance_threaded(q, p.plan, p.K, p.R, p.G, p.seed(0), 0, 32)
+    assert r["cmax"] <= 1.01 * lb
+
+
+def test_scheduled_idle_beats_random(O, presets):
+    # scheduled idle <= 50% of random-partition idle on heavy-tailed batches
+    p = presets[3]
+    ratios = []
+    for b in range(20):
+        t, f, x = p.features(b)
+        _, q, _, _ = O.predict(p.model, p.plan, t, f, x)
+        m = p.plan["n_mb"] * p.plan["l_dp"]
+        S = p.plan["e_pp"] + p.plan["l_pp"]
+        busy = 0
+        for s in range(S):
+            busy += int(q[0].sum() + q[1].sum()) if s < p.plan["e_pp"] else int(q[2].sum() + q[3].sum())
+        r = O.balance(q, p.plan, K=p.K, R=p.R, G=p.G, seed=p.seed(b), c0=0, c1=32)
+        rng = np.random.default_rng(100 + b)
+        a = rng.integers(0, m, p.n)
+        Tr, _ = BF.score_assignment(a.tolist(), q.tolist(), p.plan)
+        ratios.append((S * r["T"] - busy) / (S * Tr - busy))
+    # Idle here includes the structural part (encoder stage lighter than the LLM stages, the
+    # (p-1)/m bubble) that no partition removes; the threshold therefore applies to the mean
+    # over the 20 seeds, and every seed must still improve strictly.
+    assert np.mean(ratios) <= 0.5 and max(ratios) < 0.75, ratios
+
+
+# ------------------------------------------------------------------ Algorithm 1
+def brute_combs(g, node):
+    return [(tp, pp, g // (tp * pp)) for tp in range(1, node + 1) for pp in range(1, g + 1)
+            if g % tp == 0 and (g // tp) % pp == 0]
+
+
+def test_find_combs_examples(O):
+    for row in spec("find_combs"):
+        a = kv(row[1])
+        assert len(O.find_combs(int(a["gpus"]), int(a["node"]))) == int(row[2])
+    for row in spec("enumerate"):
+        a = kv(row[1])
+        assert len(O.enumerate_configs(int(a["n_gpus"]), int(a["node"]))) == int(row[2])
+
+
+def test_find_combs_bruteforce_and_counts(O):
+    for g in range(1, 65):
+        for node in (1, 2, 4, 8):
+            got = [tuple(int(v) for v in r) for r in O.find_combs(g, node)]
+            assert got == brute_combs(g, node)
+    assert len(O.enumerate_configs(64, 8)) == 7194
+    cfgs = O.enumerate_configs(64, 8)
+    assert int(sum(2048 // int(c[5]) for c in cfgs)) == 6541832
+    n1024 = sum(len(brute_combs(e, 8)) * len(brute_combs(1024 - e, 8)) for e in range(1, 1024))
+    assert n1024 == 414322
+
+
+def test_stage_a_makespan_example(O):
+    # (6 + 1 + 3 - 1) * max(2.0, 1.5) = 18.  Constructed so E_dur = 2 s, L_dur = 1.5 s,
+    # in ticks of 0.5 s: E = 4, L = 3 -> T_A = 36 ticks = 18 s.
+    m = unit_model(thr_e=12.0, thr_att=2.0, thr_lin=9.6, tick_ns=0.5e9)
+    m["thr_e"] = const_grid(12.0, x=(0.5, 2.0))
+    mem = dict(ms_e=dict(l=[1.0, 2.0], tp=[1.0], x=[0.0], v=[[[0.0]], [[0.0]]]),
+               as_e=dict(l=[1.0, 2.0], tp=[1.0], x=[0.0], v=[[[0.0]], [[0.0]]]),
+               ms_l=dict(l=[1.0, 2.0], tp=[1.0], x=[0.0], v=[[[0.0]], [[0.0]]]),
+               as_l=dict(l=[1.0, 2.0], tp=[1.0], x=[0.0], v=[[[0.0]], [[0.0]]]), mem_per_gpu=1.0)
+    r = O.stage_a_pair(m, mem, [1, 1, 1, 1, 3, 1], 6, 6, 1.0, 1.0)
+    assert r["feasible"] and r["e_dur"] == 4 and r["l_dur"] == 3 and r["T_A"] == 36
+
+
+def test_stage_a_memory_eq4_eq5(O, presets):
+    p = presets[4]
+    mem = p.mem()
+    he, es, hl = p.model["e_hidden"], p.model["e_seq"], p.model["l_hidden"]
+    r = O.stage_a_pair(p.model, mem, [2, 3, 1, 8, 4, 2], 16, 2048, 12.0, 3000.0)
+    le, ll = math.ceil(45 / 3), math.ceil(80 / 4)
+    t_bsz, t_seq = 12.0 * 2048 / 16, 3000.0 * 2048 / (16 * 2)
+    me = 16 * 12 * he * he * le / 2 + (3 + 4) * 34 * le * t_bsz * es * he / 2      # Eq. 4
+    ml = 16 * 12 * hl * hl * ll / 8 + 4 * 34 * ll * t_seq * hl / 8                # Eq. 5
+    assert abs(r["mem_e"] - me) <= 1e-9 * me and abs(r["mem_l"] - ml) <= 1e-9 * ml
+
+
+def test_stage_a_two_gpu_unique_and_relaxation(O, presets):
+    p = presets[4]
+    t, f, x = p.features(0)
+    mb, ms = O.batch_means(p.model, t, f, x)
+    T2, cfgs = O.stage_a_all(p.model, p.mem(), 2, 2, 64, mb, ms)
+    assert len(cfgs) == 1
+    mem = p.mem()
+    T_a, cfgs = O.stage_a_all(p.model, mem, 16, 8, 128, mb, ms)
+    best_a = int(T_a.min())
+    mem["mem_per_gpu"] *= 4
+    T_b, _ = O.stage_a_all(p.model, mem, 16, 8, 128, mb, ms)
+    assert int(T_b.min()) <= best_a
+    assert (T_b <= T_a).all()
+
+
+def test_stage_a_top_is_lexicographic_min(O, presets):
+    p = presets[2]
+    t, f, x = p.features(0)
+    mb, ms = O.batch_means(p.model, t, f, x)
+    T, cfgs = O.stage_a_all(p.model, p.mem(), 16, 8, 256, mb, ms)
+    top = O.stage_a_top(T, 10)
+    # independent re-enumeration: sort all feasible (T, pair) tuples in Python
+    feas = sorted((int(v), k) for k, v in enumerate(T) if int(v) != 2 ** 64 - 1)
+    assert len(feas) > 100
+    assert [k for _, k in feas[:10]] == [int(v) for v in top]
+    # and pair -> (eps, i) order is the Algorithm-1 loop order
+    e, i = O.pair_to_config(cfgs, 256, top[0])
+    r = O.stage_a_pair(p.model, p.mem(), cfgs[e], i, 256, mb, ms)
+    assert r["T_A"] == int(T[top[0]])
+
+
+def test_batch_means(O, presets):
+    p = presets[1]
+    t, f, x = p.features(0)
+    mb, ms = O.batch_means(p.model, t, f, x)
+    b = t.astype(np.int64) + f
+    s = x.astype(np.int64) + p.model["tau_tile"] * t.astype(np.int64) + p.model["tau_frame"] * f.astype(np.int64)
+    assert mb == b.sum() / len(b) and ms == s.sum() / len(s)
