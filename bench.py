@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""bench.py -- DFLOP plan-candidate evaluation on B200 (contract: DESIGN.md section 8).
+
+One step = one pass of the whole hot path over one synthetic global batch: a1 predict,
+a2 order, a3/a4 every candidate of the family (LPT + swap refinement + 1F1B score), a5
+argmin (NCCL min all-reduce + broadcast of the winner for N > 1) and the winner's
+assignment, through the C-ABI call ``dflop_search_plans``.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl dflop|reference]
+
+N > 1 is launched by torchrun (one rank per GPU).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate plans evaluated/sec and p50 plan latency per global batch, 1/2/4/8 B200"
+UNIT = "candidate plans/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, help="BASELINE.json config (1-based)")
+    ap.add_argument("--impl", choices=["dflop", "reference"], default="dflop")
+    ap.add_argument("--K", type=int, default=0, help="override the family size")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle baseline budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------- workload
+def workload(args, world):
+    from paper_2603_25120_b200 import synth
+    p = synth.presets()[args.config]
+    if p.plan is None:
+        raise SystemExit("config 4 (Algorithm-1 search) is benchmarked with --config 4 via tests; use 1,2,3,5")
+    K = args.K or p.K
+    scaling = "strong"
+    if p.K_scaling == "weak":
+        K = K * world
+        scaling = "weak"
+    m = p.plan["n_mb"] * p.plan["l_dp"]
+    S = p.plan["e_pp"] + p.plan["l_pp"]
+    return p, K, scaling, m, S
+
+
+def algorithmic_ops_per_candidate(n, m, S, R, G):
+    """Integer ops the method must execute per candidate:
+    LPT n*m probes x 5 ops; refinement R*(n/m)*(n/m+1) pair evaluations x 8 ops;
+    1F1B 2*S*m op updates x 4 ops; Philox-4x32-10 draws ceil(n/G)*ceil((G-1)/4) x 80 ops."""
+    per = n / max(m, 1)
+    lpt = 5.0 * n * m
+    ref = 8.0 * R * per * (per + 1)
+    sim = 4.0 * 2 * S * m
+    philox = 80.0 * (-(-n // G)) * (-(-(G - 1) // 4))
+    return lpt + ref + sim + philox
+
+
+# ---------------------------------------------------------------- clocks (NVML)
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device: int, period: float = 0.05):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self.period = period
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reasons |= int(r)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+def oracle_rate(p, K_family, budget_s, threads=None):
+    """The oracle as it stands, on the host cores: predict + candidates over a bounded sample of
+    the same workload.  Returns (candidates/s, sample description, threads used)."""
+    from oracle import oracle as O
+    threads = threads or os.cpu_count() or 1
+    t, f, x = p.features(0)
+    t0 = time.perf_counter()
+    _, q, st, _ = O.predict(p.model, p.plan, t, f, x)
+    t_pred = time.perf_counter() - t0
+    pilot = threads * 2
+    t0 = time.perf_counter()
+    O.balance_threaded(q, p.plan, K_family, p.R, p.G, p.seed(0), 0, pilot, threads=threads, per_candidate=False)
+    dt = time.perf_counter() - t0
+    n = max(pilot, min(K_family, int(pilot * budget_s / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    O.balance_threaded(q, p.plan, K_family, p.R, p.G, p.seed(0), 0, n, threads=threads, per_candidate=False)
+    dt = time.perf_counter() - t0 + t_pred
+    return n / dt, f"candidates [0, {n}) of batch 0 (+ predict of all {p.n} samples), {dt:.1f} s", threads
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    p, K, scaling, m, S = workload(args, world)
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    steps, warm = args.steps, args.warmup
+    per_step_budget = max(2.0, min(20.0, 150.0 / max(1, steps + warm)))
+    rates = []
+    for i in range(warm + steps):
+        r, sample, thr = oracle_rate(p, K, per_step_budget, threads)
+        if i >= warm:
+            rates.append(r)
+    value = statistics.mean(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "warmup": warm, "ms_per_step": 1e3 * K / value, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "R": p.R, "G": p.G,
+                   "note": "reference arm = the CPU oracle (no installable reference: the paper ships no code)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"each step: {sample}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- the GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_25120_b200 import dflop as D
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p, K, scaling, m, S = workload(args, world)
+    comm = D.Comm(rank, world, dev.index) if world > 1 else None
+    n_batches = 8
+    host = [p.features(b) for b in range(n_batches)]
+    to_dev = lambda a: torch.from_numpy(a.astype(np.uint32).view(np.int32)).to(dev)
+    dfeat = [tuple(to_dev(a) for a in h) for h in host]
+    ws = D.Workspace()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(b):
+        t, f, x = dfeat[b % n_batches]
+        return D.search_plans(p.model, t, f, x, K=K, R=p.R, G=p.G, seed=p.seed(b % n_batches), plan=p.plan,
+                              comm=comm, want_assign=True, ws=ws)
+
+    for i in range(max(3, args.warmup)):
+        step(i)
+    torch.cuda.synchronize()
+    # ---- timed region (device time, CUDA events on the launching stream)
+    D.profile_read(reset=True)
+    D.profile_enable(True)
+    times = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flushed between timed iterations
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = step(args.warmup + i)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    D.profile_enable(False)
+    prof = D.profile_read(reset=True)
+    total_ms = sum(times)
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        lat = torch.tensor(times, dtype=torch.float64, device=dev)
+        dist.all_reduce(lat, op=dist.ReduceOp.MAX)
+        times = lat.tolist()
+    value = K * args.steps / (total_ms / 1e3)          # whole-job candidates per second
+    ms_per_step = total_ms / args.steps
+    p50 = statistics.median(times)
+    p99 = float(np.percentile(np.array(times), 99))
+
+    # ---- e2e: the public call with host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        pinned = [tuple(torch.from_numpy(a.astype(np.uint32).view(np.int32)).pin_memory() for a in h) for h in host]
+        dbuf = tuple(torch.empty(p.n, dtype=torch.int32, device=dev) for _ in range(3))
+        out_host = torch.empty(p.n, dtype=torch.int32).pin_memory()
+        e_times = []
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for d_, h_ in zip(dbuf, pinned[i % n_batches]):
+                d_.copy_(h_, non_blocking=True)
+            r = D.search_plans(p.model, *dbuf, K=K, R=p.R, G=p.G, seed=p.seed(i % n_batches), plan=p.plan,
+                               comm=comm, want_assign=True, ws=ws)
+            out_host.copy_(r["assign"], non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            if i >= args.warmup:
+                e_times.append(e0.elapsed_time(e1))
+        e_total = sum(e_times)
+        if world > 1:
+            tt = torch.tensor([e_total], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_total = float(tt.item())
+        e2e = {"value": K * len(e_times) / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": 3 * 4 * p.n,
+               "d2h_bytes_per_step": 4 * p.n + 32 + 8, "p50_ms": statistics.median(e_times)}
+
+    # ---- roofline of the dominant kernel (candidates: integer-issue bound)
+    b, e = (K * rank) // world, (K * (rank + 1)) // world
+    ops_launch = algorithmic_ops_per_candidate(p.n, m, S, p.R, p.G) * (e - b)
+    cand_ms = prof["cand_ms"] / max(1, prof["cand_launches"])
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_tops = n_sm * 4 * 32 * sm_max * 1e6 / 1e12        # issue-limited int32 lane-ops
+    achieved = ops_launch / (cand_ms / 1e3) / 1e12
+    roofline = {"bound": "alu", "kernel": "k_candidates<u32>", "achieved": achieved, "peak": peak_tops,
+                "unit": "Tops/s", "frac": achieved / peak_tops, "traffic": None,
+                "kernel_ms": cand_ms, "kernel_share_of_step": cand_ms / ms_per_step,
+                "peak_note": f"{n_sm} SM x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+                "ops_per_candidate": algorithmic_ops_per_candidate(p.n, m, S, p.R, p.G)}
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        tr = json.load(open(traffic_file)).get(p.name)
+        if tr:
+            roofline["traffic"] = tr
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "K_per_gpu": K // world, "R": p.R,
+                   "G": p.G, "plan": p.plan, "tick_ns": p.model["tick_ns"],
+                   "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"candidate-shard x{world}"},
+        "p50_plan_latency_ms": p50, "p99_plan_latency_ms": p99,
+        "candidate_microbatches_per_s": value * m,
+        "e2e": e2e,
+        "gpu_launches": int(prof["kernel_launches"]),
+        "roofline": roofline,
+        "clocks": clk.summary(),
+        "winner": {"cand": res["cand"], "makespan_ticks": res["makespan"], "cmax_ticks": res["cmax"]},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sample, thr = oracle_rate(p, K, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,328 @@
+/*
+ * dflop.h -- C ABI of libdflop.so, the B200-native (sm_100a) hot path of DFLOP
+ * (arXiv 2603.25120, "DFLOP: A Data-driven Framework for Multimodal LLM Training
+ * Pipeline Optimization").
+ *
+ * The library evaluates training-plan candidates for one global batch:
+ *   a1 predict   per-sample stage costs from data features
+ *   a2 order     the LPT base order
+ *   a3 balance   seeded LPT + pairwise-swap partitions into m = N_mb * L_dp buckets
+ *                (problem statement: the scheduler ILP)
+ *   a4 score     non-interleaved 1F1B makespan of each partition (Fig. 1)
+ *   a5 argmin    over candidates (and over GPUs through NCCL)
+ *   a6 search    Algorithm 1 over (TP, PP, DP) x N_mb, then a1-a5 on the best plans
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; Rk = DESIGN.md reading k.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns a dflop_status; no C++ exception crosses the ABI.
+ *   - On a validation error nothing is launched and no output is written;
+ *     dflop_last_error() (thread-local) describes the first violated condition.
+ *   - "device" pointers are CUDA global-memory pointers on the current device
+ *     (e.g. torch tensor data_ptr()); "host" pointers are ordinary memory.  The
+ *     library never retains a caller pointer after return and never frees one.
+ *   - stream is a cudaStream_t passed as void*; NULL = the legacy default stream.
+ *   - Time is an integer count of ticks of cost_model.tick_ns nanoseconds (R19):
+ *     per-sample stage costs are u32, sums and makespans u64.
+ *   - Limits: n <= 65535 samples, m = n_mb * l_dp <= 65535 buckets, S = e_pp + l_pp
+ *     <= 32 stages, K <= 2^24 candidates, makespan < 2^40 ticks.
+ *   - Structs that carry struct_size must have it set to sizeof(struct) (versioning).
+ */
+#ifndef DFLOP_H
+#define DFLOP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFLOP_ABI_VERSION 1u
+
+typedef int32_t dflop_status;
+#define DFLOP_OK 0
+#define DFLOP_ERR_INVALID_ARGUMENT 1
+#define DFLOP_ERR_SHAPE 2
+#define DFLOP_ERR_OVERFLOW 3
+#define DFLOP_ERR_INFEASIBLE 4
+#define DFLOP_ERR_CUDA 5
+#define DFLOP_ERR_NCCL 6
+#define DFLOP_ERR_WORKSPACE_TOO_SMALL 7
+#define DFLOP_ERR_UNSUPPORTED 8
+
+/* Device status word bits (written by kernels into a caller-provided u32). */
+#define DFLOP_DEV_COST_OVERFLOW 1u     /* a predicted cost rounded to >= 2^32 ticks  */
+#define DFLOP_DEV_MAKESPAN_OVERFLOW 2u /* a makespan >= 2^40 ticks (packed argmin key) */
+
+typedef void* dflop_stream_t; /* cudaStream_t */
+
+#define DFLOP_MAX_X 32
+#define DFLOP_MAX_TP 4
+
+/* A profiled throughput grid X(x, tp) in FLOP/s per GPU (Model Profiler).
+ * Interpolation is clamped multilinear (R3).  x: shape knots (encoder effective batch b
+ * or LLM sequence length s), strictly increasing; tp: TP-degree knots, strictly
+ * increasing; v[a][k] > 0 is the value at (x[k], tp[a]). */
+typedef struct dflop_grid {
+    uint32_t n_x;  /* 1..32 */
+    uint32_t n_tp; /* 1..4  */
+    double x[DFLOP_MAX_X];
+    double tp[DFLOP_MAX_TP];
+    double v[DFLOP_MAX_TP][DFLOP_MAX_X];
+} dflop_grid;
+
+/* A profiled memory grid M(l, tp, x) in bytes (Memory Profiling): two layer
+ * counts l[0] < l[1] (linear in between and beyond), TP knots and shape knots (n_x = 1
+ * for model-state grids, which do not depend on the input shape). */
+typedef struct dflop_mem_grid {
+    uint32_t n_x;
+    uint32_t n_tp;
+    double l[2];
+    double tp[DFLOP_MAX_TP];
+    double x[DFLOP_MAX_X];
+    double v[2][DFLOP_MAX_TP][DFLOP_MAX_X];
+} dflop_mem_grid;
+
+/* The MLLM cost model (Table 1 symbols; FLOP accounting R1). */
+typedef struct dflop_cost_model {
+    uint32_t struct_size;
+    uint32_t e_layers;   /* E_l                                                 */
+    uint32_t e_hidden;   /* encoder hidden size h_E                             */
+    uint32_t e_seq;      /* E_seq_len: tokens per encoder instance      */
+    uint32_t e_attn;     /* 1 = add in-instance attention 4*h_E*E_seq^2 FLOPs   */
+    uint32_t l_layers;   /* L_l                                                 */
+    uint32_t l_hidden;   /* LLM hidden size h_L                                 */
+    uint32_t tau_tile;   /* LLM tokens contributed by one image tile            */
+    uint32_t tau_frame;  /* LLM tokens contributed by one video frame           */
+    uint32_t reserved;
+    double bwd_ratio;    /* backward / forward duration (2.0)            */
+    double tick_ns;      /* integer time unit, ns (> 0)                         */
+    dflop_grid thr_e;    /* E_thr(b, E_tp)                                      */
+    dflop_grid thr_att;  /* L_attn_thr(s, L_tp)                                 */
+    dflop_grid thr_lin;  /* L_lin_thr(s, L_tp)                                  */
+} dflop_cost_model;
+
+/* Memory model for Eq. (4)-(5). */
+typedef struct dflop_mem_model {
+    uint32_t struct_size;
+    uint32_t reserved;
+    dflop_mem_grid ms_e; /* model_state_E(l, E_tp)        */
+    dflop_mem_grid as_e; /* act_state_E(l, E_tp, b)       */
+    dflop_mem_grid ms_l; /* model_state_L(l, L_tp)        */
+    dflop_mem_grid as_l; /* act_state_L(l, L_tp, s)       */
+    double mem_per_gpu;  /* M_gpu, bytes                  */
+} dflop_mem_model;
+
+/* theta = (E_tp, E_pp, E_dp, L_tp, L_pp, L_dp, N_mb).  Buckets m = N_mb * L_dp
+ * (P:695); bucket j runs on LLM replica j % L_dp as microbatch slot j / L_dp (R10). */
+typedef struct dflop_plan {
+    uint32_t e_tp, e_pp, e_dp, l_tp, l_pp, l_dp, n_mb;
+} dflop_plan;
+
+/* The modelled cluster of Algorithm 1 (N_gpus, N_gpu_node; M_gpu is in dflop_mem_model). */
+typedef struct dflop_cluster {
+    uint32_t struct_size;
+    uint32_t n_gpus;
+    uint32_t gpus_per_node;
+    uint32_t reserved;
+} dflop_cluster;
+
+#define DFLOP_MODE_HEURISTIC 0u  /* the seeded LPT + swap-refinement family       */
+#define DFLOP_MODE_EXHAUSTIVE 1u /* candidate c = base-m digits of c (m^n <= K)    */
+
+/* Candidate family.  c = 0: the paper's LPT (current-load rule,
+ * P:738); c = 1: resulting-max LPT (R12); c >= 2: Philox-perturbed order, resulting-max
+ * LPT, then R swap-refinement rounds.  This call evaluates c in [cand_begin, cand_end). */
+typedef struct dflop_balance_params {
+    uint32_t struct_size;
+    uint32_t mode;       /* DFLOP_MODE_*                              */
+    uint32_t K;          /* family size, 1..2^24                      */
+    uint32_t cand_begin; /* shard of the family evaluated by the call */
+    uint32_t cand_end;
+    uint32_t R;          /* refinement rounds (<= 4096)               */
+    uint32_t G;          /* perturbation group size, 1..16            */
+    uint32_t seed[2];    /* Philox-4x32-10 key                        */
+    uint32_t id_base;    /* added to c in the packed argmin key       */
+} dflop_balance_params;
+
+/* Device-resident result of dflop_balance_microbatches (the argmin over the shard). */
+typedef struct dflop_cand_result {
+    uint64_t key;      /* (makespan << 24) | (id_base + c*): the packed argmin key  */
+    uint64_t makespan; /* T of the winner, ticks                                    */
+    uint64_t cmax;     /* C_max = max_j max(E_j, L_j) of the winner         */
+    uint32_t cand;     /* c* (lowest id among equal makespans, R18)                 */
+    uint32_t status;   /* DFLOP_DEV_* bits                                          */
+} dflop_cand_result;
+
+#define DFLOP_SEARCH_FIXED 0u /* theta given: Stage B only (configs with a fixed plan) */
+#define DFLOP_SEARCH_ALG1 1u  /* Algorithm 1 Stage A over all (config, N_mb), then B   */
+
+typedef struct dflop_search_params {
+    uint32_t struct_size;
+    uint32_t mode;         /* DFLOP_SEARCH_*                                   */
+    dflop_plan fixed_plan; /* used when mode == DFLOP_SEARCH_FIXED             */
+    uint32_t gbs;          /* GBS of Algorithm 1 (0 = n)                       */
+    uint32_t top_p;        /* P plans balanced in Stage B (ALG1), 1..256       */
+    uint32_t K;            /* candidates per plan, 1..2^24 (P * K < 2^24)      */
+    uint32_t R;
+    uint32_t G;
+    uint32_t seed[2];
+} dflop_search_params;
+
+/* Host-resident result of dflop_search_plans; identical on every rank. */
+typedef struct dflop_plan_result {
+    uint32_t struct_size;
+    uint32_t status_bits;       /* DFLOP_DEV_* bits seen on any rank                  */
+    dflop_plan plan;            /* theta*, N_mb included                              */
+    uint32_t m;                 /* buckets of theta*                                  */
+    uint32_t cand;              /* c* within the plan's family                        */
+    uint32_t stage_a_rank;      /* Stage-A rank of theta* (0 in FIXED mode)           */
+    uint32_t owner_rank;        /* rank whose shard held c*                           */
+    uint64_t makespan;          /* T_B of the winner, ticks                           */
+    uint64_t cmax;              /* C_max of the winner, ticks                         */
+    uint64_t stage_a_makespan;  /* T_A of theta* (0 in FIXED mode)                    */
+    dflop_plan alg1_plan;       /* Algorithm 1's literal answer (Stage-A rank 0)      */
+    uint32_t reserved;
+    uint64_t alg1_makespan;     /* its T_A                                            */
+    uint64_t n_configs;         /* |P_configs| (phase 1)                              */
+    uint64_t n_pairs;           /* (config, N_mb) pairs evaluated (phase 2)           */
+    uint64_t n_feasible;        /* pairs passing Eq. (4)-(5)                          */
+    uint64_t n_candidates;      /* candidates scored across all ranks                 */
+} dflop_plan_result;
+
+typedef struct dflop_comm dflop_comm; /* opaque NCCL communicator owned by the library */
+
+/* ---------------------------------------------------------------- support */
+uint32_t dflop_abi_version(void);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* dflop_last_error(void);
+
+/* Releases library-owned device caches (1F1B slot programs, config tables). */
+dflop_status dflop_release_caches(void);
+
+/* ---------------------------------------------------------------- instrumentation
+ * A process-wide counter of every kernel the library launches, and (when enabled) CUDA
+ * events recorded on the launching stream around each candidate-kernel launch (a3/a4),
+ * so that a benchmark can time the dominant kernel live.  dflop_profile_read synchronises
+ * the recorded events, fills *out and, if reset != 0, clears the counters. */
+typedef struct dflop_profile {
+    uint32_t struct_size;
+    uint32_t cand_launches;   /* candidate-kernel launches timed                      */
+    uint64_t kernel_launches; /* all libdflop kernel launches since the last reset    */
+    double cand_ms;           /* summed device time of the timed candidate launches   */
+} dflop_profile;
+dflop_status dflop_profile_enable(int on);
+dflop_status dflop_profile_read(dflop_profile* out, int reset);
+
+/* ---------------------------------------------------------------- a1 predict
+ * Per-sample stage costs (O1-O4 of DESIGN.md section 4):
+ *   b_i = tiles_i + frames_i                       encoder effective batch
+ *   s_i = text_i + tau_tile*tiles_i + tau_frame*frames_i   packed LLM length
+ *   ef_i = 1e9 * b_i*E_l*(24 h_E^2 E_seq [+ 4 h_E E_seq^2]) / (E_thr(b_i,E_tp)*E_tp*E_pp) * L_dp/E_dp
+ *   lf_i = 1e9 * (4 h_L L_l s_i^2 / L_attn_thr(s_i,L_tp) + 24 h_L^2 L_l s_i / L_lin_thr(s_i,L_tp))
+ *          / (L_tp*L_pp)
+ *   eb_i = bwd_ratio*ef_i, lb_i = bwd_ratio*lf_i     (ns)
+ * computed in fp32.  Outputs (device, row-major [4][n], rows ef, eb, lf, lb):
+ *   cost_f32   durations in ticks as fp32 (NULL to skip);
+ *   cost_ticks round-half-even to u32 ticks (NULL to skip); a value that rounds to
+ *              >= 2^32 is written as 0xFFFFFFFF and sets DFLOP_DEV_COST_OVERFLOW in
+ *              *dev_status (device u32, may be NULL; bits are OR-ed, never cleared).
+ * Inputs tiles/frames/text: device u32[n].  model/plan: host, copied during the call.
+ * Asynchronous on stream.
+ * Errors: INVALID_ARGUMENT (NULL model/plan, a zero degree, tick_ns <= 0, bwd_ratio < 0,
+ * a grid with non-increasing knots, a non-positive throughput value, n_x/n_tp out of
+ * range); SHAPE (n > 2^31 - 1); CUDA (launch failure). */
+dflop_status dflop_predict_costs(const dflop_cost_model* model, const dflop_plan* plan, const uint32_t* tiles,
+                                 const uint32_t* frames, const uint32_t* text, uint32_t n, float* cost_f32,
+                                 uint32_t* cost_ticks, uint32_t* dev_status, dflop_stream_t stream);
+
+/* ---------------------------------------------------------------- a2-a5 balance
+ * Partition n samples into m = n_mb*l_dp buckets with the candidate family
+ * of dflop_balance_params, score every candidate by its 1F1B makespan over S = e_pp+l_pp
+ * stages (stages < e_pp take the bucket's encoder sums, the rest its LLM sums; R7), and
+ * return the lexicographic minimum of (makespan, id_base + c) over [cand_begin, cand_end).
+ *   cost_ticks     device u32 [4][n] (rows ef, eb, lf, lb), e.g. from dflop_predict_costs.
+ *   plan           host; only e_pp, l_pp, l_dp, n_mb are used.
+ *   ws / ws_bytes  workspace query: ws == NULL stores the required size in *ws_bytes
+ *                  and returns OK without launching; otherwise ws must be a device
+ *                  buffer of at least *ws_bytes bytes, 256-byte aligned.
+ *   best           device dflop_cand_result (written).
+ *   assign         device u32[n] or NULL: bucket of every sample for c*.
+ *   group_offsets  device u32[m+1] or NULL, group_items device u32[n] or NULL: the
+ *                  winner's index groups, bucket-major, samples ascending.
+ *   cand_makespan, cand_cmax  device u64[cand_end - cand_begin] or NULL: every
+ *                  candidate's makespan / C_max (parity tests).
+ * n == 0 is allowed (every bucket empty, makespan 0); n < m leaves buckets empty.
+ * Asynchronous on stream.
+ * Errors: INVALID_ARGUMENT (m == 0, any degree 0, K == 0 or > 2^24, an empty or
+ * out-of-range shard, G outside 1..16, EXHAUSTIVE with m^n > K); SHAPE (n > 65535,
+ * m > 65535, S > 32); WORKSPACE_TOO_SMALL; UNSUPPORTED (per-candidate state larger
+ * than shared memory); CUDA. */
+dflop_status dflop_balance_microbatches(const uint32_t* cost_ticks, uint32_t n, const dflop_plan* plan,
+                                        const dflop_balance_params* bp, void* ws, size_t* ws_bytes,
+                                        dflop_cand_result* best, uint32_t* assign, uint32_t* group_offsets,
+                                        uint32_t* group_items, uint64_t* cand_makespan, uint64_t* cand_cmax,
+                                        dflop_stream_t stream);
+
+/* ---------------------------------------------------------------- a4 simulate
+ * Batched non-interleaved 1F1B (Fig. 1; R9: stage s runs w_s = min(S-1-s, M)
+ * warm-up forwards, then alternates F/B, then drains; F(s,k) after F(s-1,k), B(s,k)
+ * after B(s+1,k), B(S-1,k) after F(S-1,k); communication is free, R8).
+ *   fwd, bwd    device u64 [C][S][M] row-major durations (ticks).
+ *   makespan    device u64 [C].
+ *   stage_busy  device u64 [C][S] or NULL: sum of F+B durations per stage.
+ * Asynchronous on stream.  Errors: SHAPE (S == 0, M == 0, S > 32, M > 65535 --
+ * SPEC "inconsistent duration matrix shape"); INVALID_ARGUMENT (NULL inputs);
+ * CUDA. */
+dflop_status dflop_simulate_1f1b(const uint64_t* fwd, const uint64_t* bwd, uint32_t C, uint32_t S, uint32_t M,
+                                 uint64_t* makespan, uint64_t* stage_busy, dflop_stream_t stream);
+
+/* ---------------------------------------------------------------- index groups
+ * CSR index groups of an assignment ("returns a set of index groups"):
+ * offsets[m+1], items[n] bucket-major with samples ascending.  Device pointers;
+ * asynchronous.  Errors: INVALID_ARGUMENT, SHAPE (an assign value >= m is undefined
+ * behaviour and is not checked on device). */
+dflop_status dflop_index_groups(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items,
+                                void* ws, size_t* ws_bytes, dflop_stream_t stream);
+
+/* ---------------------------------------------------------------- a6 search
+ * One global batch end to end, synchronous on stream: a1-a5 for a fixed theta
+ * (DFLOP_SEARCH_FIXED), or Algorithm 1 Stage A over every
+ * (E_tp,E_pp,E_dp,L_tp,L_pp,L_dp) x N_mb in 1..GBS//L_dp with the Eq. (4)-(5) memory
+ * filter and the closed-form T = (N_mb + E_pp + L_pp - 1) * max(E_dur, L_dur) at the
+ * batch-mean shapes, then Stage B: a1-a5 on the batch for the top_p pairs
+ * by (T_A, config index, N_mb); the final plan minimises (T_B, Stage-A rank, c).
+ *   cl, cm, mm     host structs (mm and cl unused in FIXED mode, may be NULL).
+ *   tiles/frames/text  device u32[n].
+ *   comm           NULL = this GPU evaluates the whole family; otherwise the family
+ *                  is sharded over the communicator's ranks (candidate ranges
+ *                  [floor(g*K/G), floor((g+1)*K/G))) and one NCCL min all-reduce
+ *                  picks the winner; every rank gets the same result and assignment.
+ *   ws / ws_bytes  workspace query as in dflop_balance_microbatches.
+ *   out            host dflop_plan_result (written).
+ *   assign         device u32[n] or NULL: the winner's bucket per sample.
+ *   stage_a_out    device u64[stage_a_cap] or NULL: T_A of every pair in enumeration
+ *                  order (UINT64_MAX = infeasible), written when stage_a_cap >= n_pairs.
+ * Errors: INFEASIBLE (no pair passes Eq. (4)-(5)); OVERFLOW (a cost or makespan out of
+ * range, from the device status); NCCL; CUDA; the argument errors of the calls above. */
+dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_cost_model* cm, const dflop_mem_model* mm,
+                                const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
+                                const dflop_search_params* sp, dflop_comm* comm, void* ws, size_t* ws_bytes,
+                                dflop_plan_result* out, uint32_t* assign, uint64_t* stage_a_out,
+                                uint64_t stage_a_cap, dflop_stream_t stream);
+
+/* ---------------------------------------------------------------- NCCL
+ * Bootstrap: rank 0 calls dflop_get_unique_id, the caller broadcasts the 128 bytes
+ * (e.g. with torch.distributed), then every rank calls dflop_comm_init with its rank,
+ * the world size and its CUDA device.  The communicator is owned by the library
+ * until dflop_comm_destroy. */
+dflop_status dflop_get_unique_id(uint8_t id[128]);
+dflop_status dflop_comm_init(const uint8_t id[128], int rank, int world, int device, dflop_comm** comm);
+dflop_status dflop_comm_destroy(dflop_comm* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFLOP_H */

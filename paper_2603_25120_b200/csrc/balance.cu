@@ -1,0 +1,466 @@
+// balance.cu -- steps a2 and a5 of the DFLOP plan-candidate path on sm_100a, plus the
+// standalone 1F1B simulator and CSR index groups; the candidate kernel (a3/a4) is in
+// candidates.cu.
+//
+//   k_prep_keys     e_i = ef+eb, l_i = lf+lb, key_i = max(e_i, l_i) (R12), batch totals
+//   k_rank_sort     LPT base order pi: key descending, index ascending (R18)
+//   k_build_items   per-position item records (base order), 32- or 64-bit sums
+//   k_finalize      winner -> dflop_cand_result + assignment
+//   k_simulate      standalone batched 1F1B (dflop_simulate_1f1b)
+//   k_group_*       CSR index groups ("returns a set of index groups")
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "cand.cuh"
+#include "internal.h"
+
+namespace dflop {
+
+DFLOP_DEV uint32_t get_apos(const uint8_t* apos, uint32_t pos, bool wide) {
+    return wide ? (uint32_t)reinterpret_cast<const uint16_t*>(apos)[pos] : (uint32_t)apos[pos];
+}
+
+// ---------------------------------------------------------------- a2: keys, order, records
+__global__ void k_init(BalanceHeader* hdr, u64* slot_key, uint32_t n_slots) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) {
+        hdr->sum_e = 0;
+        hdr->sum_l = 0;
+        hdr->max_key = 0;
+        hdr->variant = 0;
+        hdr->shift = 0;
+        hdr->status = 0;
+        hdr->best_key = ~0ull;
+    }
+    for (uint32_t s = t; s < n_slots; s += gridDim.x * blockDim.x) slot_key[s] = ~0ull;
+}
+
+__global__ void k_prep_keys(const uint32_t* __restrict__ cost, uint32_t n, BalanceHeader* hdr, u64* keys) {
+    u64 se = 0, sl = 0, mk = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const u64 e = (u64)cost[i] + cost[(size_t)n + i];
+        const u64 l = (u64)cost[2 * (size_t)n + i] + cost[3 * (size_t)n + i];
+        const u64 k = e > l ? e : l;
+        keys[i] = k;
+        se += e;
+        sl += l;
+        mk = k > mk ? k : mk;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        se += __shfl_xor_sync(0xFFFFFFFFu, se, off);
+        sl += __shfl_xor_sync(0xFFFFFFFFu, sl, off);
+        const u64 o = __shfl_xor_sync(0xFFFFFFFFu, mk, off);
+        mk = o > mk ? o : mk;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&hdr->sum_e, se);
+        atomicAdd(&hdr->sum_l, sl);
+        atomicMax(&hdr->max_key, mk);
+    }
+}
+
+// rank_i = #{j : key_j > key_i or (key_j == key_i and j < i)}; order[rank_i] = i.
+__global__ void k_rank_sort(const u64* __restrict__ keys, uint32_t n, uint32_t* order, uint32_t* item_pos) {
+    __shared__ u64 tile[256];
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u64 ki = i < n ? keys[i] : 0;
+    uint32_t rank = 0;
+    for (uint32_t base = 0; base < n; base += 256) {
+        __syncthreads();
+        if (base + threadIdx.x < n) tile[threadIdx.x] = keys[base + threadIdx.x];
+        __syncthreads();
+        const uint32_t lim = min(256u, n - base);
+        if (i < n) {
+            for (uint32_t u = 0; u < lim; ++u) {
+                const u64 kj = tile[u];
+                rank += (kj > ki) | ((kj == ki) & (base + u < i));
+            }
+        }
+    }
+    if (i < n) {
+        order[rank] = i;
+        item_pos[i] = rank;
+    }
+}
+
+// Chooses the candidate-kernel variant and writes the per-position records.
+//   u32 when every bucket sum fits (sums of all e_i, l_i below 2^32 - 1);
+//   packed u32 when moreover every LPT bucket load stays below 2^(32 - s), s = bits of m - 1:
+//   a probe's winner has W <= min_j W_j + max(e, l) <= (sum_e + sum_l)/m + max key, every
+//   probe adds at most one more max key, and refinement never raises the maximum (O6).
+__global__ void k_build_items(const uint32_t* __restrict__ cost, uint32_t n, uint32_t m, uint32_t allow_pack,
+                              BalanceHeader* hdr, const uint32_t* __restrict__ order, ItemRec<uint32_t>* it32,
+                              ItemRec<u64>* it64) {
+    const bool fits = hdr->sum_e < 0xFFFFFFFFull && hdr->sum_l < 0xFFFFFFFFull;
+    uint32_t sh = 0;
+    while ((1u << sh) < m) ++sh;
+    const u64 bound = (hdr->sum_e + hdr->sum_l + m - 1) / m + 2 * hdr->max_key;
+    const bool packed = allow_pack && fits && sh < 32 && bound < (1ull << (32 - sh));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        hdr->variant = packed ? 0u : (fits ? 1u : 2u);
+        hdr->shift = sh;
+    }
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const uint32_t i = order[t];
+        const uint32_t ef = cost[i], eb = cost[(size_t)n + i], lf = cost[2 * (size_t)n + i],
+                       lb = cost[3 * (size_t)n + i];
+        if (fits)
+            it32[t] = ItemRec<uint32_t>{ef + eb, lf + lb, ef, lf};
+        else
+            it64[t] = ItemRec<u64>{(u64)ef + eb, (u64)lf + lb, (u64)ef, (u64)lf};
+    }
+}
+
+// ---------------------------------------------------------------- a5: winner
+__global__ void k_finalize(BalanceHeader* hdr, const u64* slot_key, const u64* slot_T, const u64* slot_cmax,
+                           const uint32_t* slot_buf, const uint8_t* slot_apos, uint32_t n_slots,
+                           uint32_t apos_bytes, uint32_t wide, const uint32_t* pos_item, uint32_t n,
+                           uint32_t id_base, dflop_cand_result* best, uint32_t* assign) {
+    __shared__ uint32_t s_slot;
+    const u64 key = hdr->best_key;
+    if (threadIdx.x == 0) s_slot = 0xFFFFFFFFu;
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < n_slots; s += blockDim.x)
+        if (slot_key[s] == key) atomicMin(&s_slot, s);
+    __syncthreads();
+    const uint32_t s = s_slot;
+    if (threadIdx.x == 0) {
+        best->key = key;
+        best->makespan = s != 0xFFFFFFFFu ? slot_T[s] : 0;
+        best->cmax = s != 0xFFFFFFFFu ? slot_cmax[s] : 0;
+        best->cand = (uint32_t)(key & 0xFFFFFFull) - id_base;
+        best->status = hdr->status;
+    }
+    if (assign && s != 0xFFFFFFFFu) {
+        const uint8_t* ap = slot_apos + ((size_t)s * 2 + slot_buf[s]) * apos_bytes;
+        for (uint32_t pos = threadIdx.x; pos < n; pos += blockDim.x)
+            assign[pos_item[pos]] = get_apos(ap, pos, wide != 0);
+    }
+}
+
+// ---------------------------------------------------------------- standalone 1F1B
+__global__ void k_simulate(const u64* __restrict__ fwd, const u64* __restrict__ bwd, uint32_t C, uint32_t S,
+                           uint32_t M, const uint32_t* __restrict__ ops, uint32_t n_ops, uint32_t D, u64* makespan,
+                           u64* busy) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const uint32_t Dm = D - 1;
+    u64* last = reinterpret_cast<u64*>(smem) + (size_t)threadIdx.x * (S + 2 * S * D);
+    u64* FR = last + S;
+    u64* BR = FR + S * D;
+    const u64* f = fwd + (size_t)c * S * M;
+    const u64* b = bwd + (size_t)c * S * M;
+    for (uint32_t s = 0; s < S; ++s) last[s] = 0;
+    for (uint32_t q = 0; q < n_ops; ++q) {
+        const uint32_t op = __ldg(ops + q);
+        const uint32_t kind = op_kind(op), s = op_stage(op), k = op_mb(op);
+        u64 dur, dep = 0;
+        if (kind == 0) {
+            dur = f[(size_t)s * M + k];
+            if (s > 0) dep = FR[(s - 1) * D + (k & Dm)];
+        } else {
+            dur = b[(size_t)s * M + k];
+            dep = (s + 1 < S) ? BR[(s + 1) * D + (k & Dm)] : FR[s * D + (k & Dm)];
+        }
+        const u64 l0 = last[s];
+        const u64 end = (l0 > dep ? l0 : dep) + dur;
+        last[s] = end;
+        if (kind == 0)
+            FR[s * D + (k & Dm)] = end;
+        else
+            BR[s * D + (k & Dm)] = end;
+    }
+    u64 T = 0;
+    for (uint32_t s = 0; s < S; ++s) T = last[s] > T ? last[s] : T;
+    makespan[c] = T;
+    if (busy) {
+        for (uint32_t s = 0; s < S; ++s) {
+            u64 acc = 0;
+            for (uint32_t k = 0; k < M; ++k) acc += f[(size_t)s * M + k] + b[(size_t)s * M + k];
+            busy[(size_t)c * S + s] = acc;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- CSR index groups
+__global__ void k_group_count(const uint32_t* __restrict__ assign, uint32_t n, uint32_t* cnt) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        atomicAdd(&cnt[assign[i]], 1u);
+}
+
+// exclusive scan of cnt[m] into offsets[m+1] and fill[m] (one block of 1024 threads)
+__global__ void k_group_scan(const uint32_t* cnt, uint32_t m, uint32_t* offsets, uint32_t* fill) {
+    __shared__ uint32_t part[1024];
+    const uint32_t t = threadIdx.x;
+    const uint32_t per = (m + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = min(m, t * per), hi = min(m, lo + per);
+    uint32_t s = 0;
+    for (uint32_t j = lo; j < hi; ++j) s += cnt[j];
+    part[t] = s;
+    __syncthreads();
+    for (uint32_t off = 1; off < blockDim.x; off <<= 1) {
+        uint32_t v = t >= off ? part[t - off] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[t] - s;
+    for (uint32_t j = lo; j < hi; ++j) {
+        offsets[j] = run;
+        fill[j] = run;
+        run += cnt[j];
+    }
+    if (t == blockDim.x - 1) offsets[m] = part[t];
+}
+
+// stable placement, samples ascending within each bucket: one warp walks the samples in
+// chunks of 32; __match_any_sync ranks equal buckets inside a chunk.
+__global__ void k_group_place(const uint32_t* __restrict__ assign, uint32_t n, uint32_t* fill, uint32_t* items) {
+    const uint32_t lane = threadIdx.x;
+    for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t i = base + lane;
+        const bool valid = i < n;
+        const uint32_t a = valid ? assign[i] : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, a);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        uint32_t at = 0;
+        if (valid) at = fill[a] + rank;
+        __syncwarp();
+        if (valid) {
+            items[at] = i;
+            if (rank == 0) fill[a] += __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- host side
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+static uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
+static uint32_t next_pow2(uint32_t x) {
+    uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+size_t groups_ws_bytes(uint32_t n, uint32_t m) {
+    (void)n;
+    return align256((size_t)m * 4) * 2;
+}
+
+cudaError_t groups_launch(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items,
+                          void* ws, cudaStream_t s) {
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(ws);
+    uint32_t* fill = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ws) + align256((size_t)m * 4));
+    cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)m * 4, s);
+    if (e != cudaSuccess) return e;
+    if (n > 0) k_group_count<<<std::min<uint32_t>((n + 255) / 256, 1184), 256, 0, s>>>(assign, n, cnt);
+    k_group_scan<<<1, 1024, 0, s>>>(cnt, m, offsets, fill);
+    if (n > 0) k_group_place<<<1, 32, 0, s>>>(assign, n, fill, items);
+    count_launches(n > 0 ? 3 : 1);
+    return cudaGetLastError();
+}
+
+
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
+BalanceConfig balance_config(const BalanceShape& sh, int device) {
+    BalanceConfig cfg;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+        cfg.why = "cudaGetDeviceProperties failed";
+        return cfg;
+    }
+    const uint32_t n = sh.n, m = sh.m, S = sh.S;
+    // lanes per candidate: about 8 buckets per lane
+    int gl = (int)next_pow2((m + 7) / 8);
+    gl = std::min(32, std::max(1, gl));
+    const int forced = env_int("DFLOP_GL", 0);
+    if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) gl = forced;
+    cfg.gl = gl;
+    const uint32_t per_bucket = (n + m - 1) / std::max(1u, m);
+    uint32_t cap = std::min(256u, std::max(32u, next_pow2(3 * std::max(1u, per_bucket))));
+    const int forced_cap = env_int("DFLOP_CAP", 0);
+    if (forced_cap >= 1 && forced_cap <= 4096) cap = (uint32_t)forced_cap;
+    cfg.cap = cap;
+    const bool wide = m > 255;
+    cfg.apos_bytes = round16(std::max(16u, n * (wide ? 2u : 1u)));
+    const uint32_t scr = round16(std::max(16u + 4u * cfg.cap, (S + 2 * S * sh.D) * 8u));
+    const size_t smem_max = prop.sharedMemPerBlockOptin;
+    const uint32_t nsm = (uint32_t)prop.multiProcessorCount;
+    const uint32_t per_warp = 32u / (uint32_t)gl;  // candidate groups per warp
+    for (int v = 0; v < 3; ++v) {
+        const uint32_t asz = v == 2 ? 8u : 4u;
+        const uint32_t el = round16(m * 2u * asz);   // EL[m] then FL[m]
+        cfg.off_fl[v] = el;
+        cfg.off_scr[v] = 2 * el;
+        uint32_t cb = 2 * el + scr;
+        // stagger consecutive candidates across banks: a group's probe touches GL*2*asz bytes
+        const uint32_t span = std::max(16u, (uint32_t)gl * 2u * asz);
+        if (span < 128) {
+            const uint32_t want = span;  // a multiple of 16 below 128: reachable in <= 7 steps
+            while (cb % 128 != want) cb += 16;
+        }
+        cfg.cand_bytes[v] = cb;
+        const uint32_t tbl = (uint32_t)(((size_t)n * (v == 2 ? 32u : 16u) + (size_t)n * 2 + 127) & ~(size_t)127);
+        // stage the table in shared memory when it leaves room for at least 2 warps of candidates
+        cfg.tbl_smem[v] = (size_t)tbl + (size_t)2 * per_warp * cb <= smem_max;
+        cfg.tbl_bytes[v] = cfg.tbl_smem[v] ? tbl : 0;
+        uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - cfg.tbl_bytes[v]) / cb, 1024 / gl);
+        // no more groups than the family needs (one CTA per SM), whole warps only
+        cpb = std::min<uint32_t>(cpb, std::max(1u, (sh.n_cand + nsm - 1) / nsm));
+        cpb = (cpb + per_warp - 1) / per_warp * per_warp;
+        if ((size_t)cfg.tbl_bytes[v] + (size_t)cpb * cb > smem_max) cpb -= per_warp;
+        if (cpb == 0) {
+            char buf[200];
+            snprintf(buf, sizeof buf,
+                     "a warp of %u candidates needs %u B of shared memory, more than %zu B (n=%u, m=%u)", per_warp,
+                     per_warp * cb, smem_max, n, m);
+            cfg.why = buf;
+            return cfg;
+        }
+        const size_t dyn = (size_t)cfg.tbl_bytes[v] + (size_t)cpb * cb;
+        cudaFuncSetAttribute(cand_kernel_ptr(v, gl, cfg.tbl_smem[v]), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dyn);
+        const uint32_t want = (sh.n_cand + cpb - 1) / cpb;
+        cfg.cpb[v] = cpb;
+        cfg.grid[v] = std::max(1u, std::min<uint32_t>(want, nsm));
+    }
+    cfg.n_slots = 0;
+    for (int v = 0; v < 3; ++v) cfg.n_slots = std::max(cfg.n_slots, cfg.grid[v] * cfg.cpb[v]);
+    if (env_int("DFLOP_DEBUG", 0))
+        fprintf(stderr,
+                "[dflop] balance n=%u m=%u S=%u D=%u gl=%d cap=%u apos=%u | packed/u32/u64: tbl=%u/%u/%u "
+                "cand=%u/%u/%u cpb=%u/%u/%u grid=%u/%u/%u | slots=%u\n",
+                n, m, S, sh.D, gl, cfg.cap, cfg.apos_bytes, cfg.tbl_bytes[0], cfg.tbl_bytes[1], cfg.tbl_bytes[2],
+                cfg.cand_bytes[0], cfg.cand_bytes[1], cfg.cand_bytes[2], cfg.cpb[0], cfg.cpb[1], cfg.cpb[2],
+                cfg.grid[0], cfg.grid[1], cfg.grid[2], cfg.n_slots);
+    size_t o = 0;
+    cfg.o_hdr = o;        o += align256(sizeof(BalanceHeader));
+    cfg.o_keys = o;       o += align256((size_t)n * 8);
+    cfg.o_order = o;      o += align256((size_t)n * 4);
+    cfg.o_item_pos = o;   o += align256((size_t)n * 4);
+    cfg.o_items32 = o;    o += align256((size_t)n * 16);
+    cfg.o_items64 = o;    o += align256((size_t)n * 32);
+    cfg.o_slot_key = o;   o += align256((size_t)cfg.n_slots * 8);
+    cfg.o_slot_T = o;     o += align256((size_t)cfg.n_slots * 8);
+    cfg.o_slot_cmax = o;  o += align256((size_t)cfg.n_slots * 8);
+    cfg.o_slot_buf = o;   o += align256((size_t)cfg.n_slots * 4);
+    cfg.o_slot_apos = o;  o += align256((size_t)cfg.n_slots * 2 * cfg.apos_bytes);
+    cfg.o_grp = o;        o += groups_ws_bytes(n, m);
+    cfg.total = o;
+    cfg.ok = true;
+    return cfg;
+}
+
+dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, const SlotProgram& prog,
+                            cudaStream_t s) {
+    char* ws = reinterpret_cast<char*>(a.ws);
+    BalanceHeader* hdr = reinterpret_cast<BalanceHeader*>(ws + cfg.o_hdr);
+    u64* keys = reinterpret_cast<u64*>(ws + cfg.o_keys);
+    uint32_t* order = reinterpret_cast<uint32_t*>(ws + cfg.o_order);
+    uint32_t* item_pos = reinterpret_cast<uint32_t*>(ws + cfg.o_item_pos);
+    auto* it32 = reinterpret_cast<ItemRec<uint32_t>*>(ws + cfg.o_items32);
+    auto* it64 = reinterpret_cast<ItemRec<u64>*>(ws + cfg.o_items64);
+    u64* slot_key = reinterpret_cast<u64*>(ws + cfg.o_slot_key);
+    u64* slot_T = reinterpret_cast<u64*>(ws + cfg.o_slot_T);
+    u64* slot_cmax = reinterpret_cast<u64*>(ws + cfg.o_slot_cmax);
+    uint32_t* slot_buf = reinterpret_cast<uint32_t*>(ws + cfg.o_slot_buf);
+    uint8_t* slot_apos = reinterpret_cast<uint8_t*>(ws + cfg.o_slot_apos);
+    const uint32_t n = a.sh.n;
+    const uint32_t allow_pack = a.sh.mode == DFLOP_MODE_EXHAUSTIVE ? 0u : 1u;
+
+    k_init<<<std::max(1u, std::min<uint32_t>((cfg.n_slots + 255) / 256, 148)), 256, 0, s>>>(hdr, slot_key,
+                                                                                          cfg.n_slots);
+    if (n > 0) {
+        const uint32_t gb = std::min<uint32_t>((n + 255) / 256, 592);
+        k_prep_keys<<<gb, 256, 0, s>>>(a.cost_ticks, n, hdr, keys);
+        k_rank_sort<<<(n + 255) / 256, 256, 0, s>>>(keys, n, order, item_pos);
+        k_build_items<<<gb, 256, 0, s>>>(a.cost_ticks, n, a.sh.m, allow_pack, hdr, order, it32, it64);
+    } else {
+        k_build_items<<<1, 32, 0, s>>>(a.cost_ticks, 0, a.sh.m, allow_pack, hdr, order, it32, it64);
+    }
+    CandParams p{};
+    p.pos_item = order;
+    p.item_pos = item_pos;
+    p.ops = prog.d_ops;
+    p.hdr = hdr;
+    p.slot_apos = slot_apos;
+    p.slot_key = slot_key;
+    p.slot_T = slot_T;
+    p.slot_cmax = slot_cmax;
+    p.slot_buf = slot_buf;
+    p.cand_T = reinterpret_cast<u64*>(a.cand_T);
+    p.cand_cmax = reinterpret_cast<u64*>(a.cand_cmax);
+    p.n = n;
+    p.m = a.sh.m;
+    p.S = a.sh.S;
+    p.e_pp = a.sh.e_pp;
+    p.l_dp = a.sh.l_dp;
+    p.n_mb = a.sh.n_mb;
+    p.R = a.sh.R;
+    p.G = a.sh.G;
+    p.D = prog.D;
+    p.n_ops = prog.n_ops;
+    p.c_begin = a.c_begin;
+    p.c_end = a.c_end;
+    p.id_base = a.id_base;
+    p.seed0 = a.seed0;
+    p.seed1 = a.seed1;
+    p.exhaustive = a.sh.mode == DFLOP_MODE_EXHAUSTIVE;
+    p.wide = a.sh.m > 255;
+    p.cap = cfg.cap;
+    p.apos_bytes = cfg.apos_bytes;
+    const int mark = prof_begin(s);
+    for (int v = 0; v < 3; ++v) {
+        CandParams q = p;
+        q.items = v == 2 ? reinterpret_cast<const void*>(it64) : reinterpret_cast<const void*>(it32);
+        q.tbl_bytes = cfg.tbl_bytes[v];
+        q.cand_bytes = cfg.cand_bytes[v];
+        q.off_fl = cfg.off_fl[v];
+        q.off_scr = cfg.off_scr[v];
+        q.want_variant = (uint32_t)v;
+        CandLaunch L;
+        L.variant = v;
+        L.gl = cfg.gl;
+        L.tbl_smem = cfg.tbl_smem[v];
+        L.grid = cfg.grid[v];
+        L.cpb = cfg.cpb[v];
+        L.dyn = (size_t)cfg.tbl_bytes[v] + (size_t)cfg.cpb[v] * cfg.cand_bytes[v];
+        cudaFuncSetAttribute(cand_kernel_ptr(v, cfg.gl, cfg.tbl_smem[v]), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)L.dyn);
+        cand_launch(L, q, s);
+        prof_mark(mark, v + 1, s);
+    }
+    k_finalize<<<1, 256, 0, s>>>(hdr, slot_key, slot_T, slot_cmax, slot_buf, slot_apos, cfg.n_slots, cfg.apos_bytes,
+                                 a.sh.m > 255, order, n, a.id_base, a.best, a.assign);
+    count_launches(n > 0 ? 8 : 6);
+    return cuda_status(cudaGetLastError(), "balance launch");
+}
+
+dflop_status simulate_launch(const uint64_t* fwd, const uint64_t* bwd, uint32_t C, uint32_t S, uint32_t M,
+                             uint64_t* makespan, uint64_t* busy, const SlotProgram& prog, cudaStream_t s) {
+    if (C == 0) return DFLOP_OK;
+    const size_t per = (size_t)(S + 2 * S * prog.D) * 8;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, dev);
+    uint32_t threads = (uint32_t)std::min<size_t>(256, prop.sharedMemPerBlockOptin / per);
+    threads = std::max(1u, std::min(threads, C));
+    const size_t dyn = per * threads;
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(&k_simulate), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)dyn);
+    k_simulate<<<(C + threads - 1) / threads, threads, dyn, s>>>(
+        reinterpret_cast<const u64*>(fwd), reinterpret_cast<const u64*>(bwd), C, S, M, prog.d_ops, prog.n_ops,
+        prog.D, reinterpret_cast<u64*>(makespan), reinterpret_cast<u64*>(busy));
+    count_launches(1);
+    return cuda_status(cudaGetLastError(), "simulate launch");
+}
+
+}  // namespace dflop

@@ -1,0 +1,49 @@
+// cand.cuh -- parameters of the candidate kernel (a3/a4) shared by its launcher and kernels.
+#pragma once
+#include "common.cuh"
+
+namespace dflop {
+
+// Kernel variants (chosen on device by k_build_items, each launch exits unless it matches):
+//   0  packed 32-bit: bucket loads stored as (E << s | j, L << s | j), s = bits of m - 1, so
+//      one probe is max(E' + e', L' + l') and the argmin is a plain min (no index compare)
+//   1  plain 32-bit sums
+//   2  64-bit sums
+constexpr int kVariants = 3;
+
+// Per-launch parameters.  Shared-memory layout (bytes):
+//   [0, tbl_bytes)              CTA item table: ItemRec<A>[n] then u16 pos->item[n]
+//   tbl_bytes + g*cand_bytes    candidate group g: EL[m] {E, L}, FL[m] {EF, LF}, scratch
+// Global: per resident group ("slot") two assignment buffers of apos_bytes (u8 per base-order
+// position when m <= 255, else u16), the best one named by slot_buf[slot].
+struct CandParams {
+    const void* items;           // ItemRec<A>[n], base-order positions (global)
+    const uint32_t* pos_item;    // [n] position -> item index (global)
+    const uint32_t* item_pos;    // [n] item index -> position (global)
+    const uint32_t* ops;         // 1F1B slot program, n_ops entries
+    BalanceHeader* hdr;
+    uint8_t* slot_apos;          // [n_slots][2][apos_bytes]
+    u64* slot_key;
+    u64* slot_T;
+    u64* slot_cmax;
+    uint32_t* slot_buf;
+    u64* cand_T;                 // optional per-candidate outputs
+    u64* cand_cmax;
+    uint32_t n, m, S, e_pp, l_dp, n_mb, R, G, D, n_ops;
+    uint32_t c_begin, c_end, id_base, seed0, seed1;
+    uint32_t exhaustive, wide, cap, apos_bytes, want_variant;
+    uint32_t tbl_bytes, cand_bytes, off_fl, off_scr;
+};
+
+struct CandLaunch {
+    int variant;      // see above
+    int gl;           // lanes per candidate
+    bool tbl_smem;    // item table staged in shared memory
+    uint32_t grid, cpb;
+    size_t dyn;
+};
+
+const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem);
+void cand_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+
+}  // namespace dflop

@@ -1,0 +1,583 @@
+// cand_impl.cuh -- the hot kernel of the path (a3 + a4): every candidate of the seeded
+// family (O6-O7) is one group of GL lanes of a warp:
+//
+//   order  Philox4x32-10 Fisher-Yates inside groups of G base-order positions (c >= 2)
+//   LPT    per sample, the argmin over m buckets of max(E_j + e_i, L_j + l_i) (c >= 1) or of
+//          the current max(E_j, L_j) (c == 0, the paper's rule); the GL lanes of the
+//          group each probe m/GL buckets and reduce (value, bucket) with warp shuffles
+//   refine R rounds: bottleneck bucket j*, Philox partner j', best move or swap
+//   score  non-interleaved 1F1B makespan over S stages, C_max
+//
+// Variants (cand.cuh): packed 32-bit keys (E << s | j, L << s | j) when the provable load bound
+// allows, plain 32-bit, or 64-bit sums.
+//
+// Memory: the per-sample records (16 B in the 32-bit variant) and the position->item map
+// are staged ONCE per CTA in shared memory and shared by all candidates of the SM; each
+// candidate keeps SoA bucket sums EL[m] = {E, L}, FL[m] = {EF, LF} and a scratch area in
+// shared memory (per-candidate stride staggered across banks); its assignment (one byte
+// per sample when m <= 255) lives in an L2-resident per-slot double buffer, written by
+// the LPT/refinement leader lane and scanned with 16-byte L2 loads by the refinement.  A
+// new per-slot best flips the buffer index instead of copying.
+#pragma once
+#include "cand.cuh"
+
+namespace dflop {
+
+// ---------------------------------------------------------------- helpers
+template <typename A>
+DFLOP_DEV A amax() {
+    return (A)~(A)0;
+}
+template <typename A>
+DFLOP_DEV A maxa(A a, A b) {
+    return a > b ? a : b;
+}
+template <typename A>
+DFLOP_DEV A shfl_x(unsigned mask, A v, int off) {
+    return __shfl_xor_sync(mask, v, off);
+}
+// Every warp is full (blockDim is a multiple of 32) and all candidate groups of a warp run
+// identical control flow, so shuffles and warp barriers use the full mask; xor offsets below
+// GL keep each exchange inside its group.
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+template <typename A, int GL>
+DFLOP_DEV void argmin_reduce(A& v, uint32_t& j, unsigned mask) {
+#pragma unroll
+    for (int off = GL / 2; off > 0; off >>= 1) {
+        const A v2 = shfl_x(mask, v, off);
+        const uint32_t j2 = __shfl_xor_sync(mask, j, off);
+        if (v2 < v || (v2 == v && j2 < j)) {
+            v = v2;
+            j = j2;
+        }
+    }
+}
+
+// (W descending, j ascending); j == UINT32_MAX marks "no bucket on this lane"
+template <typename A, int GL>
+DFLOP_DEV void argmax_reduce(A& w, uint32_t& j, unsigned mask) {
+#pragma unroll
+    for (int off = GL / 2; off > 0; off >>= 1) {
+        const A w2 = shfl_x(mask, w, off);
+        const uint32_t j2 = __shfl_xor_sync(mask, j, off);
+        const bool take = (j2 != 0xFFFFFFFFu) && (j == 0xFFFFFFFFu || w2 > w || (w2 == w && j2 < j));
+        if (take) {
+            w = w2;
+            j = j2;
+        }
+    }
+}
+
+template <typename A, int GL>
+DFLOP_DEV A max_reduce(A v, unsigned mask) {
+#pragma unroll
+    for (int off = GL / 2; off > 0; off >>= 1) v = maxa(v, shfl_x(mask, v, off));
+    return v;
+}
+
+template <typename A, int GL>
+DFLOP_DEV void lexmin_reduce(A& s, uint32_t& i, uint32_t& r, unsigned mask) {
+#pragma unroll
+    for (int off = GL / 2; off > 0; off >>= 1) {
+        const A s2 = shfl_x(mask, s, off);
+        const uint32_t i2 = __shfl_xor_sync(mask, i, off);
+        const uint32_t r2 = __shfl_xor_sync(mask, r, off);
+        if (s2 < s || (s2 == s && (i2 < i || (i2 == i && r2 < r)))) {
+            s = s2;
+            i = i2;
+            r = r2;
+        }
+    }
+}
+
+template <typename A>
+DFLOP_DEV void lex_update(A& bs, uint32_t& bi, uint32_t& br, A s, uint32_t i, uint32_t r) {
+    if (s < bs || (s == bs && (i < bi || (i == bi && r < br)))) {
+        bs = s;
+        bi = i;
+        br = r;
+    }
+}
+
+// Fisher-Yates permutation of the ng <= 16 positions of group g for candidate c, packed as
+// nibbles (nibble t = offset placed at position t).  Words u[0], u[1], ... come from
+// Philox(ctr = (g, c, 0, p)), word q of call p being u[4p+q]; step t = ng-1 .. 1 uses
+// u[ng-1-t] and swaps t with mulhi32(u, t+1).
+DFLOP_DEV uint64_t make_perm(uint32_t g, uint32_t c, uint32_t ng, uint32_t k0, uint32_t k1) {
+    uint64_t perm = 0xFEDCBA9876543210ull;
+    Philox4 w{0, 0, 0, 0};
+    for (uint32_t idx = 0; idx + 1 < ng; ++idx) {
+        const uint32_t q = idx & 3u;
+        if (q == 0) w = philox4x32_10(g, c, 0u, idx >> 2, k0, k1);
+        const uint32_t u = q == 0 ? w.x : q == 1 ? w.y : q == 2 ? w.z : w.w;
+        const uint32_t t = ng - 1 - idx;
+        const uint32_t r = mulhi32(u, t + 1);
+        const uint64_t a = (perm >> (4 * t)) & 15ull, b = (perm >> (4 * r)) & 15ull;
+        const uint64_t x = a ^ b;
+        perm ^= (x << (4 * t)) | (x << (4 * r));
+    }
+    return perm;
+}
+
+// ---------------------------------------------------------------- item table access
+template <typename A, bool SM>
+struct Tbl {
+    const ItemRec<A>* it;
+    const uint16_t* pi16;   // SM
+    const uint32_t* pi32;   // !SM
+    DFLOP_DEV ItemRec<A> item(uint32_t pos) const {
+        if (SM) return it[pos];
+        if (sizeof(A) == 4) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(it) + pos);
+            return ItemRec<A>{(A)v.x, (A)v.y, (A)v.z, (A)v.w};
+        }
+        const ulonglong2* q = reinterpret_cast<const ulonglong2*>(it) + 2 * (size_t)pos;
+        const ulonglong2 a = __ldg(q), b = __ldg(q + 1);
+        return ItemRec<A>{(A)a.x, (A)a.y, (A)b.x, (A)b.y};
+    }
+    DFLOP_DEV Pair2<A> el(uint32_t pos) const {
+        if (SM) return *reinterpret_cast<const Pair2<A>*>(it + pos);
+        const ItemRec<A> r = item(pos);
+        return Pair2<A>{r.e, r.l};
+    }
+    DFLOP_DEV uint32_t idx(uint32_t pos) const { return SM ? (uint32_t)pi16[pos] : __ldg(pi32 + pos); }
+};
+
+// load of bucket j without the packed index bits
+template <typename A, bool PK>
+DFLOP_DEV A unpack(A v, uint32_t sh) {
+    return PK ? (A)(v >> sh) : v;
+}
+
+DFLOP_DEV void set_apos(uint8_t* apos, uint32_t pos, uint32_t j, bool wide) {
+    if (wide)
+        reinterpret_cast<uint16_t*>(apos)[pos] = (uint16_t)j;
+    else
+        apos[pos] = (uint8_t)j;
+}
+
+// Processes one 16-byte block of the assignment (16 positions u8 / 8 positions u16) and calls
+// f(pos, which) for every position assigned to ja (which = 0) or jb (which = 1).
+template <typename F>
+DFLOP_DEV void scan_words(const uint4 v, uint32_t blk, bool wide, uint32_t ja, uint32_t jb, F&& f) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if (!wide) {
+        const uint32_t A4 = ja * 0x01010101u, B4 = jb * 0x01010101u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t ea = __vcmpeq4(w[k], A4), eb = __vcmpeq4(w[k], B4);
+            while (ea | eb) {
+                const uint32_t e = ea ? ea : eb;
+                const int which = ea ? 0 : 1;
+                const int byte = (__ffs(e) - 1) >> 3;
+                f(blk * 16 + 4 * k + byte, which);
+                if (which == 0) ea &= ~(0xFFu << (8 * byte)); else eb &= ~(0xFFu << (8 * byte));
+            }
+        }
+    } else {
+        const uint32_t A2 = ja * 0x00010001u, B2 = jb * 0x00010001u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t ea = __vcmpeq2(w[k], A2), eb = __vcmpeq2(w[k], B2);
+            while (ea | eb) {
+                const uint32_t e = ea ? ea : eb;
+                const int which = ea ? 0 : 1;
+                const int half = (__ffs(e) - 1) >> 4;
+                f(blk * 8 + 2 * k + half, which);
+                if (which == 0) ea &= ~(0xFFFFu << (16 * half)); else eb &= ~(0xFFFFu << (16 * half));
+            }
+        }
+    }
+}
+
+template <typename F>
+DFLOP_DEV void scan_block(const uint8_t* apos, uint32_t blk, bool wide, uint32_t ja, uint32_t jb, F&& f) {
+    scan_words(__ldcg(reinterpret_cast<const uint4*>(apos) + blk), blk, wide, ja, jb, f);
+}
+
+// ---------------------------------------------------------------- LPT pass (R12)
+// c == 0: argmin of the current max(E_j, L_j) (the paper's rule); c >= 1: argmin of the
+// resulting max(E_j + e_i, L_j + l_i); lowest j on ties.
+template <typename A, bool PK, int GL, bool SM>
+DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
+                        Pair2<A>* FL, uint8_t* apos, uint32_t gl) {
+    const uint32_t n = p.n, m = p.m, G = p.G;
+    const bool wide = p.wide != 0;
+    const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
+    const uint32_t jmask = (1u << sh) - 1u;
+    uint32_t g = 0;
+    for (uint32_t start = 0; start < n; start += G, ++g) {
+        const uint32_t ng = min(G, n - start);
+        const uint64_t perm = (c >= 2 && ng > 1) ? make_perm(g, c, ng, p.seed0, p.seed1) : 0xFEDCBA9876543210ull;
+        for (uint32_t t = 0; t < ng; ++t) {
+            const uint32_t pos = start + (uint32_t)((perm >> (4 * t)) & 15ull);
+            const ItemRec<A> it = T.item(pos);
+            uint32_t bj;
+            if (PK) {
+                // keys (W << s) | j: one fused add-max and one min per probe
+                const uint32_t es = ((uint32_t)it.e << sh) & (uint32_t)use, ls = ((uint32_t)it.l << sh) & (uint32_t)use;
+                uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
+                uint32_t j = gl;
+#pragma unroll 4
+                for (; j + GL < m; j += 2 * GL) {
+                    const Pair2<A> x = EL[j], y = EL[j + GL];
+                    b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                    b1 = min(b1, max((uint32_t)y.a + es, (uint32_t)y.b + ls));
+                }
+                if (j < m) {
+                    const Pair2<A> x = EL[j];
+                    b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                }
+                uint32_t best = min(b0, b1);
+#pragma unroll
+                for (int off = GL / 2; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(FULL, best, off));
+                bj = best & jmask;
+            } else {
+                const A ae = it.e & use, al = it.l & use;
+                A bv = amax<A>();
+                bj = 0xFFFFFFFFu;
+#pragma unroll 4
+                for (uint32_t j = gl; j < m; j += GL) {
+                    const Pair2<A> el = EL[j];
+                    const A v = maxa<A>(el.a + ae, el.b + al);
+                    if (v < bv) {
+                        bv = v;
+                        bj = j;
+                    }
+                }
+                argmin_reduce<A, GL>(bv, bj, FULL);
+            }
+            if (gl == 0) {
+                Pair2<A> el = EL[bj], fl = FL[bj];
+                el.a += PK ? (A)((uint32_t)it.e << sh) : it.e;
+                el.b += PK ? (A)((uint32_t)it.l << sh) : it.l;
+                fl.a += it.ef;
+                fl.b += it.lf;
+                EL[bj] = el;
+                FL[bj] = fl;
+                set_apos(apos, pos, bj, wide);
+            }
+            __syncwarp(FULL);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- swap refinement (O6)
+// `apply` is false for c < 2: the rounds are still executed (and discarded) so that every
+// group of a warp issues the same shuffle sequence.
+template <typename A, bool PK, int GL, bool SM>
+DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
+                      uint8_t* apos, uint8_t* scr, uint32_t gl, bool apply) {
+    const uint32_t m = p.m, cap = p.cap;
+    const bool wide = p.wide != 0;
+    const uint32_t nblk = p.apos_bytes / 16;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(scr);
+    uint16_t* ls = reinterpret_cast<uint16_t*>(scr + 16);
+    uint16_t* lp = ls + cap;
+    for (uint32_t r = 0; r < p.R; ++r) {
+        // bottleneck bucket j* = lowest j with maximal W_j = max(E_j, L_j)
+        A Wb = 0;
+        uint32_t jb = 0xFFFFFFFFu;
+        for (uint32_t j = gl; j < m; j += GL) {
+            const Pair2<A> el = EL[j];
+            const A W = unpack<A, PK>(maxa(el.a, el.b), sh);
+            if (jb == 0xFFFFFFFFu || W > Wb) {
+                Wb = W;
+                jb = j;
+            }
+        }
+        argmax_reduce<A, GL>(Wb, jb, FULL);
+        const uint32_t js = jb;
+        const A Ws = Wb;
+        const Philox4 w = philox4x32_10(r, c, 1u, 0u, p.seed0, p.seed1);
+        const uint32_t jp = (js + 1u + mulhi32(w.x, m - 1u)) % m;
+        const Pair2<A> Bsp = EL[js], Bpp = EL[jp];
+        const Pair2<A> Bs{unpack<A, PK>(Bsp.a, sh), unpack<A, PK>(Bsp.b, sh)};
+        const Pair2<A> Bp{unpack<A, PK>(Bpp.a, sh), unpack<A, PK>(Bpp.b, sh)};
+        if (gl == 0) {
+            cnt[0] = 0;
+            cnt[1] = 0;
+        }
+        __syncwarp(FULL);
+        // member lists of j* (ls) and j' (lp): 16-byte L2 scans of the assignment, 4 in flight
+        for (uint32_t b0 = gl; b0 < nblk; b0 += 4 * GL) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t b = b0 + u * GL;
+                v[u] = b < nblk ? __ldcg(reinterpret_cast<const uint4*>(apos) + b) : make_uint4(~0u, ~0u, ~0u, ~0u);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                scan_words(v[u], b0 + u * GL, wide, js, jp, [&](uint32_t pos, int which) {
+                    const uint32_t at = atomicAdd(&cnt[which], 1u);
+                    if (at < cap) (which ? lp : ls)[at] = (uint16_t)pos;
+                });
+        }
+        __syncwarp(FULL);
+        const uint32_t nA = cnt[0], nB = cnt[1];
+        __syncwarp(FULL);
+        A bsc = amax<A>();
+        uint32_t bi = 0xFFFFFFFFu, brk = 0xFFFFFFFFu;
+        u64 bkey = ~0ull;  // 32-bit scores: (score << 32 | item << 16 | rank), a branch-free min
+        // all (i, i') with i in j*, i' in {NONE} u j'; lexicographic min of (score, i, rank(i'))
+        auto eval_i = [&](uint32_t pi) {
+            const Pair2<A> a = T.el(pi);
+            const uint32_t ii = T.idx(pi);
+            const A se = Bs.a - a.a, sl = Bs.b - a.b;  // j* without i
+            const A pe = Bp.a + a.a, pl = Bp.b + a.b;  // j' with i
+            const A s0 = maxa(maxa(se, sl), maxa(pe, pl));
+            if (sizeof(A) == 4)
+                bkey = min(bkey, ((u64)s0 << 32) | ((u64)ii << 16));
+            else
+                lex_update(bsc, bi, brk, s0, ii, 0u);
+            auto pair = [&](uint32_t pj) {
+                const Pair2<A> b = T.el(pj);
+                const uint32_t rk = T.idx(pj) + 1u;
+                const A s1 = maxa<A>(se + b.a, sl + b.b);
+                const A s2 = maxa<A>(pe - b.a, pl - b.b);
+                if (sizeof(A) == 4)
+                    bkey = min(bkey, ((u64)maxa(s1, s2) << 32) | ((u64)ii << 16) | rk);
+                else
+                    lex_update(bsc, bi, brk, maxa(s1, s2), ii, rk);
+            };
+            if (nB <= cap) {
+                for (uint32_t v = 0; v < nB; ++v) pair(lp[v]);
+            } else {
+                for (uint32_t bb = 0; bb < nblk; ++bb)
+                    scan_block(apos, bb, wide, jp, jp, [&](uint32_t pos, int which) {
+                        if (which == 0) pair(pos);
+                    });
+            }
+        };
+        if (nA <= cap) {
+            for (uint32_t u = gl; u < nA; u += GL) eval_i(ls[u]);
+        } else {
+            for (uint32_t b = gl; b < nblk; b += GL)
+                scan_block(apos, b, wide, js, js, [&](uint32_t pos, int which) {
+                    if (which == 0) eval_i(pos);
+                });
+        }
+        if (sizeof(A) == 4) {
+#pragma unroll
+            for (int off = GL / 2; off > 0; off >>= 1) bkey = min(bkey, __shfl_xor_sync(FULL, bkey, off));
+            if (bkey != ~0ull) {
+                bsc = (A)(bkey >> 32);
+                bi = (uint32_t)(bkey >> 16) & 0xFFFFu;
+                brk = (uint32_t)bkey & 0xFFFFu;
+            }
+        } else {
+            lexmin_reduce<A, GL>(bsc, bi, brk, FULL);
+        }
+        if (apply && gl == 0 && bi != 0xFFFFFFFFu && bsc < Ws) {
+            const uint32_t pi = __ldg(p.item_pos + bi);
+            const ItemRec<A> a = T.item(pi);
+            const A ae = PK ? (A)((uint32_t)a.e << sh) : a.e, al = PK ? (A)((uint32_t)a.l << sh) : a.l;
+            Pair2<A> es = EL[js], fs = FL[js], ep = EL[jp], fp = FL[jp];
+            es.a -= ae; es.b -= al; fs.a -= a.ef; fs.b -= a.lf;
+            ep.a += ae; ep.b += al; fp.a += a.ef; fp.b += a.lf;
+            set_apos(apos, pi, jp, wide);
+            if (brk != 0u) {
+                const uint32_t pj = __ldg(p.item_pos + (brk - 1u));
+                const ItemRec<A> b = T.item(pj);
+                const A be = PK ? (A)((uint32_t)b.e << sh) : b.e, bl = PK ? (A)((uint32_t)b.l << sh) : b.l;
+                ep.a -= be; ep.b -= bl; fp.a -= b.ef; fp.b -= b.lf;
+                es.a += be; es.b += bl; fs.a += b.ef; fs.b += b.lf;
+                set_apos(apos, pj, js, wide);
+            }
+            EL[js] = es;
+            FL[js] = fs;
+            EL[jp] = ep;
+            FL[jp] = fp;
+        }
+        __syncwarp(FULL);
+    }
+}
+
+// ---------------------------------------------------------------- 1F1B score (O7)
+// Replica rho runs buckets j = k*L_dp + rho as slots k (R10); stages < E_pp take (EF, E-EF),
+// the rest (LF, L-LF) (R7).  Ops in the host-built topological order, rings of depth D.
+template <typename A, bool PK>
+DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr) {
+    const uint32_t S = p.S, D = p.D, Dm = p.D - 1;
+    u64* last = scr;
+    u64* FR = scr + S;
+    u64* BR = FR + S * D;
+    u64 T = 0;
+    for (uint32_t rho = 0; rho < p.l_dp; ++rho) {
+        for (uint32_t s = 0; s < S; ++s) last[s] = 0;
+        for (uint32_t q = 0; q < p.n_ops; ++q) {
+            const uint32_t op = __ldg(p.ops + q);
+            const uint32_t kind = op_kind(op), s = op_stage(op), k = op_mb(op);
+            const uint32_t j = k * p.l_dp + rho;
+            const Pair2<A> el = EL[j], fl = FL[j];
+            const bool enc = s < p.e_pp;
+            u64 dur, dep = 0;
+            if (kind == 0) {
+                dur = enc ? (u64)fl.a : (u64)fl.b;
+                if (s > 0) dep = FR[(s - 1) * D + (k & Dm)];
+            } else {
+                dur = enc ? (u64)(unpack<A, PK>(el.a, sh) - fl.a) : (u64)(unpack<A, PK>(el.b, sh) - fl.b);
+                dep = (s + 1 < S) ? BR[(s + 1) * D + (k & Dm)] : FR[s * D + (k & Dm)];
+            }
+            const u64 l0 = last[s];
+            const u64 end = (l0 > dep ? l0 : dep) + dur;
+            last[s] = end;
+            if (kind == 0)
+                FR[s * D + (k & Dm)] = end;
+            else
+                BR[s * D + (k & Dm)] = end;
+        }
+        for (uint32_t s = 0; s < S; ++s) T = last[s] > T ? last[s] : T;
+    }
+    return T;
+}
+
+template <typename A, bool PK, int GL, bool SM>
+DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
+                             Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint32_t gl, u64& Tc, u64& cmax) {
+    const uint32_t m = p.m;
+    for (uint32_t j = gl; j < m; j += GL) {
+        EL[j] = PK ? Pair2<A>{(A)j, (A)j} : Pair2<A>{0, 0};
+        FL[j] = Pair2<A>{0, 0};
+    }
+    __syncwarp(FULL);
+    if (p.exhaustive) {
+        // candidate c = base-m digits: a_i = floor(c / m^i) mod m (never packed)
+        if (gl == 0) {
+            uint32_t x = c;
+            for (uint32_t i = 0; i < p.n; ++i) {
+                const uint32_t d = x % m;
+                x /= m;
+                const uint32_t pos = __ldg(p.item_pos + i);
+                const ItemRec<A> it = T.item(pos);
+                EL[d].a += it.e;
+                EL[d].b += it.l;
+                FL[d].a += it.ef;
+                FL[d].b += it.lf;
+                set_apos(apos, pos, d, p.wide != 0);
+            }
+        }
+        __syncwarp(FULL);
+    } else {
+        lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, gl);
+        if (m >= 2) refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, gl, c >= 2);
+    }
+    A cm = 0;
+    for (uint32_t j = gl; j < m; j += GL) {
+        const Pair2<A> el = EL[j];
+        cm = maxa(cm, unpack<A, PK>(maxa(el.a, el.b), sh));
+    }
+    cmax = (u64)max_reduce<A, GL>(cm, FULL);
+    Tc = (gl == 0) ? score_1f1b<A, PK>(p, sh, EL, FL, reinterpret_cast<u64*>(scr)) : 0;
+    __syncwarp(FULL);
+}
+
+template <typename A, bool PK, int GL, bool SM>
+__global__ void __launch_bounds__(1024) k_candidates(CandParams p) {
+    if (p.hdr->variant != p.want_variant) return;  // another variant runs
+    const uint32_t sh = PK ? p.hdr->shift : 0u;
+    extern __shared__ __align__(128) uint8_t smem[];
+    Tbl<A, SM> T;
+    if (SM) {
+        const uint32_t words = p.n * (uint32_t)sizeof(ItemRec<A>) / 16;
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
+            reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.items) + i);
+        uint16_t* pi16 = reinterpret_cast<uint16_t*>(smem + (size_t)p.n * sizeof(ItemRec<A>));
+        for (uint32_t i = threadIdx.x; i < p.n; i += blockDim.x) pi16[i] = (uint16_t)__ldg(p.pos_item + i);
+        __syncthreads();
+        T.it = reinterpret_cast<const ItemRec<A>*>(smem);
+        T.pi16 = pi16;
+        T.pi32 = nullptr;
+    } else {
+        T.it = reinterpret_cast<const ItemRec<A>*>(p.items);
+        T.pi16 = nullptr;
+        T.pi32 = p.pos_item;
+    }
+    const uint32_t grp = threadIdx.x / GL, gl = threadIdx.x % GL;
+    const uint32_t cpb = blockDim.x / GL;
+    uint8_t* base = smem + p.tbl_bytes + (size_t)grp * p.cand_bytes;
+    Pair2<A>* EL = reinterpret_cast<Pair2<A>*>(base);
+    Pair2<A>* FL = reinterpret_cast<Pair2<A>*>(base + p.off_fl);
+    uint8_t* scr = base + p.off_scr;
+    const uint32_t slot = blockIdx.x * cpb + grp;
+    uint8_t* bufs = p.slot_apos + (size_t)slot * 2 * p.apos_bytes;
+    // padding past n never matches a bucket (0xFF / 0xFFFF)
+    const uint32_t used = p.n * (p.wide ? 2u : 1u);
+    for (uint32_t b = used + gl; b < p.apos_bytes; b += GL) {
+        bufs[b] = 0xFF;
+        bufs[p.apos_bytes + b] = 0xFF;
+    }
+    __syncwarp(FULL);
+    uint32_t cur = 0, best_buf = 0;
+    u64 best_key = ~0ull, best_T = 0, best_cmax = 0;
+    for (uint32_t c0 = p.c_begin + blockIdx.x * cpb; c0 < p.c_end; c0 += gridDim.x * cpb) {
+        const bool valid = c0 + grp < p.c_end;
+        const uint32_t c = valid ? c0 + grp : p.c_end - 1;  // tail groups recompute a real candidate
+        uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
+        u64 Tc, cmax;
+        run_candidate<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, gl, Tc, cmax);
+        Tc = __shfl_sync(FULL, Tc, 0, GL);
+        u64 key;
+        if (Tc >= (1ull << 40)) {
+            if (gl == 0) atomicOr(&p.hdr->status, (uint32_t)DFLOP_DEV_MAKESPAN_OVERFLOW);
+            key = (((1ull << 40) - 1) << 24) | (u64)(p.id_base + c);
+        } else {
+            key = (Tc << 24) | (u64)(p.id_base + c);
+        }
+        if (!valid) continue;
+        if (gl == 0 && p.cand_T) {
+            p.cand_T[c - p.c_begin] = Tc;
+            p.cand_cmax[c - p.c_begin] = cmax;
+        }
+        if (key < best_key) {  // keep this buffer, write the next candidate into the other
+            best_key = key;
+            best_T = Tc;
+            best_cmax = cmax;
+            best_buf = cur;
+            cur ^= 1u;
+        }
+    }
+    if (gl == 0) {
+        p.slot_key[slot] = best_key;
+        p.slot_T[slot] = best_T;
+        p.slot_cmax[slot] = best_cmax;
+        p.slot_buf[slot] = best_buf;
+        if (best_key != ~0ull) atomicMin(&p.hdr->best_key, best_key);
+    }
+}
+
+template <typename A, bool PK, bool SM>
+static const void* ptr_gl(int gl) {
+    switch (gl) {
+        case 1: return reinterpret_cast<const void*>(&k_candidates<A, PK, 1, SM>);
+        case 2: return reinterpret_cast<const void*>(&k_candidates<A, PK, 2, SM>);
+        case 4: return reinterpret_cast<const void*>(&k_candidates<A, PK, 4, SM>);
+        case 8: return reinterpret_cast<const void*>(&k_candidates<A, PK, 8, SM>);
+        case 16: return reinterpret_cast<const void*>(&k_candidates<A, PK, 16, SM>);
+        default: return reinterpret_cast<const void*>(&k_candidates<A, PK, 32, SM>);
+    }
+}
+
+template <typename A, bool PK, bool SM>
+static void launch_gl(const CandLaunch& L, const CandParams& p, cudaStream_t s) {
+    const dim3 grid(L.grid), block(L.cpb * L.gl);
+    switch (L.gl) {
+        case 1: k_candidates<A, PK, 1, SM><<<grid, block, L.dyn, s>>>(p); break;
+        case 2: k_candidates<A, PK, 2, SM><<<grid, block, L.dyn, s>>>(p); break;
+        case 4: k_candidates<A, PK, 4, SM><<<grid, block, L.dyn, s>>>(p); break;
+        case 8: k_candidates<A, PK, 8, SM><<<grid, block, L.dyn, s>>>(p); break;
+        case 16: k_candidates<A, PK, 16, SM><<<grid, block, L.dyn, s>>>(p); break;
+        default: k_candidates<A, PK, 32, SM><<<grid, block, L.dyn, s>>>(p); break;
+    }
+}
+
+// one translation unit per (variant, table placement) so the 36 instantiations build in parallel
+#define DFLOP_CAND_UNIT(NAME, A, PK, SM)                                                         \
+    const void* cand_ptr_##NAME(int gl) { return ptr_gl<A, PK, SM>(gl); }                         \
+    void cand_launch_##NAME(const CandLaunch& L, const CandParams& p, cudaStream_t s) {           \
+        launch_gl<A, PK, SM>(L, p, s);                                                            \
+    }
+
+}  // namespace dflop

@@ -1,0 +1,109 @@
+// internal.h -- host-side declarations shared by the libdflop translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dflop.h"
+
+namespace dflop {
+
+void set_error(const char* fmt, ...);
+
+// instrumentation (profile.cpp)
+void count_launches(uint32_t k);
+bool profiling();
+// returns an index to pass to prof_mark(); -1 when profiling is off
+int prof_begin(cudaStream_t s);
+void prof_mark(int idx, int which, cudaStream_t s);  // which: 1 = between variants, 2 = end
+dflop_status cuda_status(cudaError_t e, const char* what);
+
+// ---------------------------------------------------------------- predict
+struct PredictConsts {
+    float scale_e, scale_att, scale_lin, bwd;
+    uint32_t tau_tile, tau_frame;
+    float tp_e, tp_l;
+};
+dflop_status validate_cost_model(const dflop_cost_model* m);
+dflop_status validate_plan(const dflop_plan* p);
+PredictConsts predict_consts(const dflop_cost_model* m, const dflop_plan* p);
+cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* consts, uint32_t n_plans,
+                           const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
+                           float* cost_f32, uint32_t* cost_ticks, size_t plan_stride, uint32_t* dev_status,
+                           cudaStream_t s);
+
+// ---------------------------------------------------------------- 1F1B slot program
+struct SlotProgram {
+    uint32_t S = 0, M = 0, D = 0;  // D = ring depth (power of two)
+    const uint32_t* d_ops = nullptr;  // device copy, 2*S*M entries
+    uint32_t n_ops = 0;
+};
+// Builds (once per (S, M) and device) a topological order of the 1F1B DAG by Kahn levels.
+dflop_status get_slot_program(uint32_t S, uint32_t M, SlotProgram* out);
+void release_slot_programs();
+
+// ---------------------------------------------------------------- balance
+struct BalanceShape {
+    uint32_t n, m, S, e_pp, l_dp, n_mb;
+    uint32_t mode, R, G;
+    uint32_t n_cand;  // cand_end - cand_begin
+    uint32_t D;       // 1F1B ring depth of the slot program
+};
+struct BalanceConfig {
+    int gl = 1;                        // lanes per candidate
+    uint32_t cap = 0;                  // refinement list capacity
+    uint32_t apos_bytes = 0;           // one assignment buffer (u8 or u16 per position)
+    // per kernel variant: [0] packed u32, [1] plain u32, [2] u64 (cand.cuh)
+    bool tbl_smem[3] = {false, false, false};  // item table staged in shared memory
+    uint32_t tbl_bytes[3] = {0, 0, 0};
+    uint32_t cand_bytes[3] = {0, 0, 0};        // per-candidate smem
+    uint32_t off_fl[3] = {0, 0, 0}, off_scr[3] = {0, 0, 0};
+    uint32_t cpb[3] = {0, 0, 0};               // candidates per block
+    uint32_t grid[3] = {0, 0, 0};
+    uint32_t n_slots = 0;
+    // workspace layout (byte offsets)
+    size_t o_hdr, o_keys, o_order, o_item_pos, o_items32, o_items64, o_slot_key, o_slot_T, o_slot_cmax,
+        o_slot_buf, o_slot_apos, o_grp, total;
+    bool ok = false;
+    std::string why;
+};
+BalanceConfig balance_config(const BalanceShape& sh, int device);
+// Launches the whole a2..a5 sequence for one plan on `stream`.
+struct BalanceArgs {
+    const uint32_t* cost_ticks;
+    BalanceShape sh;
+    uint32_t K, c_begin, c_end, seed0, seed1, id_base;
+    void* ws;
+    dflop_cand_result* best;
+    uint32_t* assign;
+    uint64_t* cand_T;
+    uint64_t* cand_cmax;
+};
+dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, const SlotProgram& prog,
+                            cudaStream_t s);
+
+dflop_status simulate_launch(const uint64_t* fwd, const uint64_t* bwd, uint32_t C, uint32_t S, uint32_t M,
+                             uint64_t* makespan, uint64_t* busy, const SlotProgram& prog, cudaStream_t s);
+
+size_t groups_ws_bytes(uint32_t n, uint32_t m);
+cudaError_t groups_launch(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items,
+                          void* ws, cudaStream_t s);
+
+// ---------------------------------------------------------------- stage A
+struct StageAConsts;  // defined in stage_a.cu
+struct StageATop {
+    uint64_t T;
+    uint32_t pair;
+    uint32_t pad;
+};
+size_t stage_a_ws_bytes(uint64_t n_pairs, int device);
+dflop_status stage_a_launch(const dflop_cost_model* cm, const dflop_mem_model* mm, const uint32_t* d_cfgs,
+                            const uint32_t* d_pair_start, uint32_t n_cfgs, uint64_t n_pairs, uint32_t gbs,
+                            const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
+                            uint32_t top_p, void* ws, uint64_t* stage_a_out, StageATop* d_top,
+                            unsigned long long* d_n_feasible, cudaStream_t s);
+
+}  // namespace dflop

@@ -1,0 +1,175 @@
+// predict.cu -- step a1: per-sample stage costs from data features.
+//
+//   b = tiles + frames, s = text + tau_tile*tiles + tau_frame*frames
+//   ef = scale_e * b / E_thr(b, E_tp)                     (0 when b == 0)
+//   lf = scale_att * s^2 / L_attn_thr(s, L_tp) + scale_lin * s / L_lin_thr(s, L_tp)
+//   eb = r * ef, lb = r * lf
+// where the host folds 1e9 * FLOPs-per-unit / (tp * pp) / tick (and L_dp / E_dp, R13) into
+// the fp32 scale constants in double precision.  One thread handles 4 consecutive samples
+// with 16-byte loads/stores: 12 B in and 32 B out per sample and plan, HBM-bound at large n.
+// Multi-plan launches (Stage B of the search) use blockIdx.y as the plan index.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace dflop {
+
+struct PredictGrids {
+    GridF e, att, lin;
+};
+
+struct PredictLaunch {
+    PredictConsts c[64];
+};
+
+DFLOP_DEV void tp_bracket(const GridF& g, float tp, int& a, float& wt) {
+    a = 0;
+    wt = 0.0f;
+    if (g.n_tp == 1) return;
+    const float th = fminf(fmaxf(tp, g.tp[0]), g.tp[g.n_tp - 1]);
+    while (a + 1 < g.n_tp - 1 && g.tp[a + 1] <= th) ++a;
+    wt = (th - g.tp[a]) / (g.tp[a + 1] - g.tp[a]);
+}
+
+DFLOP_DEV uint32_t to_ticks(float v, uint32_t& ovf) {
+    if (!(v < 4294967296.0f)) {
+        ovf = 1;
+        return 0xFFFFFFFFu;
+    }
+    return __float2uint_rn(v);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaunch L, const uint32_t* __restrict__ tiles,
+                                                 const uint32_t* __restrict__ frames, const uint32_t* __restrict__ text,
+                                                 uint32_t n, float* cost_f32, uint32_t* cost_ticks, size_t plan_stride,
+                                                 uint32_t* dev_status) {
+    __shared__ PredictGrids g;
+    for (uint32_t w = threadIdx.x; w < sizeof(PredictGrids) / 4; w += blockDim.x)
+        reinterpret_cast<uint32_t*>(&g)[w] = reinterpret_cast<const uint32_t*>(&grids)[w];
+    __syncthreads();
+    const PredictConsts k = L.c[blockIdx.y];
+    int ae, aa, al;
+    float we, wa, wl;
+    tp_bracket(g.e, k.tp_e, ae, we);
+    tp_bracket(g.att, k.tp_l, aa, wa);
+    tp_bracket(g.lin, k.tp_l, al, wl);
+    float* f32 = cost_f32 ? cost_f32 + (size_t)blockIdx.y * plan_stride : nullptr;
+    uint32_t* tk = cost_ticks ? cost_ticks + (size_t)blockIdx.y * plan_stride : nullptr;
+    uint32_t ovf = 0;
+    const uint32_t nq = VEC ? n / 4 : n;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+        uint32_t tv[4], fv[4], xv[4];
+        const int cnt = VEC ? 4 : 1;
+        if (VEC) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(tiles) + q);
+            const uint4 b = __ldg(reinterpret_cast<const uint4*>(frames) + q);
+            const uint4 c = __ldg(reinterpret_cast<const uint4*>(text) + q);
+            tv[0] = a.x; tv[1] = a.y; tv[2] = a.z; tv[3] = a.w;
+            fv[0] = b.x; fv[1] = b.y; fv[2] = b.z; fv[3] = b.w;
+            xv[0] = c.x; xv[1] = c.y; xv[2] = c.z; xv[3] = c.w;
+        } else {
+            tv[0] = __ldg(tiles + q);
+            fv[0] = __ldg(frames + q);
+            xv[0] = __ldg(text + q);
+        }
+        float o[4][4];
+        uint32_t t4[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (u >= cnt) break;
+            const float b = (float)((u64)tv[u] + fv[u]);
+            const float s = (float)((u64)xv[u] + (u64)k.tau_tile * tv[u] + (u64)k.tau_frame * fv[u]);
+            float ef = 0.0f;
+            if (b > 0.0f) ef = (k.scale_e * b) / interp_grid_f(g.e, b, ae, we);
+            const float lf = (k.scale_att * s * s) / interp_grid_f(g.att, s, aa, wa) +
+                             (k.scale_lin * s) / interp_grid_f(g.lin, s, al, wl);
+            o[0][u] = ef;
+            o[1][u] = k.bwd * ef;
+            o[2][u] = lf;
+            o[3][u] = k.bwd * lf;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) t4[r][u] = to_ticks(o[r][u], ovf);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (VEC) {
+                if (f32) reinterpret_cast<float4*>(f32 + (size_t)r * n)[q] = make_float4(o[r][0], o[r][1], o[r][2], o[r][3]);
+                if (tk) reinterpret_cast<uint4*>(tk + (size_t)r * n)[q] = make_uint4(t4[r][0], t4[r][1], t4[r][2], t4[r][3]);
+            } else {
+                if (f32) f32[(size_t)r * n + q] = o[r][0];
+                if (tk) tk[(size_t)r * n + q] = t4[r][0];
+            }
+        }
+    }
+    if (ovf && dev_status) atomicOr(dev_status, (uint32_t)DFLOP_DEV_COST_OVERFLOW);
+}
+
+static void to_gridf(const dflop_grid& s, GridF& d) {
+    d.n_x = (int)s.n_x;
+    d.n_tp = (int)s.n_tp;
+    for (int k = 0; k < DFLOP_MAX_X; ++k) d.x[k] = k < (int)s.n_x ? (float)s.x[k] : 0.0f;
+    for (int a = 0; a < DFLOP_MAX_TP; ++a) {
+        d.tp[a] = a < (int)s.n_tp ? (float)s.tp[a] : 0.0f;
+        for (int k = 0; k < DFLOP_MAX_X; ++k) d.v[a][k] = (a < (int)s.n_tp && k < (int)s.n_x) ? (float)s.v[a][k] : 0.0f;
+    }
+}
+
+PredictConsts predict_consts(const dflop_cost_model* m, const dflop_plan* p) {
+    // FLOP accounting R1: 24*h^2 per token and layer (linear), 4*h*s^2 attention.
+    const double lin_e = 24.0 * (double)m->e_hidden * (double)m->e_hidden;
+    const double att_e = m->e_attn ? 4.0 * (double)m->e_hidden : 0.0;
+    const double per_inst_e = lin_e * (double)m->e_seq + att_e * (double)m->e_seq * (double)m->e_seq;
+    const double c_e = (double)m->e_layers * per_inst_e;
+    const double c_lin = 24.0 * (double)m->l_hidden * (double)m->l_hidden * (double)m->l_layers;
+    const double c_att = 4.0 * (double)m->l_hidden * (double)m->l_layers;
+    PredictConsts k;
+    // divide by thr * tp * pp; R13: encoder time per LLM bucket x L_dp / E_dp
+    k.scale_e = (float)(1e9 * c_e / ((double)p->e_tp * (double)p->e_pp) * ((double)p->l_dp / (double)p->e_dp) /
+                        m->tick_ns);
+    k.scale_att = (float)(1e9 * c_att / ((double)p->l_tp * (double)p->l_pp) / m->tick_ns);
+    k.scale_lin = (float)(1e9 * c_lin / ((double)p->l_tp * (double)p->l_pp) / m->tick_ns);
+    k.bwd = (float)m->bwd_ratio;
+    k.tau_tile = m->tau_tile;
+    k.tau_frame = m->tau_frame;
+    k.tp_e = (float)p->e_tp;
+    k.tp_l = (float)p->l_tp;
+    return k;
+}
+
+cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* consts, uint32_t n_plans,
+                           const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
+                           float* cost_f32, uint32_t* cost_ticks, size_t plan_stride, uint32_t* dev_status,
+                           cudaStream_t s) {
+    if (n == 0 || n_plans == 0) return cudaSuccess;
+    PredictGrids g;
+    to_gridf(m->thr_e, g.e);
+    to_gridf(m->thr_att, g.att);
+    to_gridf(m->thr_lin, g.lin);
+    const bool vec = (n % 4 == 0) && ((uintptr_t)tiles % 16 == 0) && ((uintptr_t)frames % 16 == 0) &&
+                     ((uintptr_t)text % 16 == 0) && (!cost_f32 || (uintptr_t)cost_f32 % 16 == 0) &&
+                     (!cost_ticks || (uintptr_t)cost_ticks % 16 == 0) && (plan_stride % 4 == 0);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t work = vec ? n / 4 : n;
+    for (uint32_t p0 = 0; p0 < n_plans; p0 += 64) {
+        const uint32_t np = std::min<uint32_t>(64, n_plans - p0);
+        PredictLaunch L;
+        for (uint32_t i = 0; i < np; ++i) L.c[i] = consts[p0 + i];
+        const uint32_t gx = std::max(1u, std::min<uint32_t>((work + 255) / 256, (uint32_t)sms * 8 / np + 1));
+        dim3 grid(gx, np);
+        float* f = cost_f32 ? cost_f32 + (size_t)p0 * plan_stride : nullptr;
+        uint32_t* t = cost_ticks ? cost_ticks + (size_t)p0 * plan_stride : nullptr;
+        if (vec)
+            k_predict<true><<<grid, 256, 0, s>>>(g, L, tiles, frames, text, n, f, t, plan_stride, dev_status);
+        else
+            k_predict<false><<<grid, 256, 0, s>>>(g, L, tiles, frames, text, n, f, t, plan_stride, dev_status);
+        count_launches(1);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace dflop

@@ -1,0 +1,83 @@
+// profile.cpp -- launch counter and CUDA-event timing of the candidate kernels.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace dflop {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+std::atomic<bool> g_on{false};
+std::mutex g_mu;
+struct Mark {
+    cudaEvent_t e[4];
+};
+std::vector<Mark> g_marks;   // recorded, not yet read
+std::vector<Mark> g_free;    // reusable events
+}  // namespace
+
+void count_launches(uint32_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+bool profiling() { return g_on.load(std::memory_order_relaxed); }
+
+int prof_begin(cudaStream_t s) {
+    if (!profiling()) return -1;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Mark m;
+    if (!g_free.empty()) {
+        m = g_free.back();
+        g_free.pop_back();
+    } else {
+        for (auto& e : m.e) cudaEventCreate(&e);
+    }
+    cudaEventRecord(m.e[0], s);
+    g_marks.push_back(m);
+    return (int)g_marks.size() - 1;
+}
+
+void prof_mark(int idx, int which, cudaStream_t s) {  // which = 1..3
+    if (idx < 0) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (idx < (int)g_marks.size()) cudaEventRecord(g_marks[idx].e[which], s);
+}
+
+}  // namespace dflop
+
+using namespace dflop;
+
+extern "C" dflop_status dflop_profile_enable(int on) {
+    g_on.store(on != 0);
+    return DFLOP_OK;
+}
+
+extern "C" dflop_status dflop_profile_read(dflop_profile* out, int reset) {
+    if (!out || out->struct_size != sizeof(dflop_profile)) {
+        set_error("dflop_profile struct_size");
+        return DFLOP_ERR_INVALID_ARGUMENT;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    double ms = 0.0;
+    for (auto& m : g_marks) {
+        cudaError_t e = cudaEventSynchronize(m.e[3]);
+        if (e != cudaSuccess) return cuda_status(e, "profile event");
+        float best = 0.f;
+        for (int v = 0; v < 3; ++v) {  // the variant that ran (the others exit at once)
+            float t = 0.f;
+            cudaEventElapsedTime(&t, m.e[v], m.e[v + 1]);
+            best = t > best ? t : best;
+        }
+        ms += best;
+    }
+    out->cand_launches = (uint32_t)g_marks.size();
+    out->kernel_launches = g_launches.load();
+    out->cand_ms = ms;
+    if (reset) {
+        for (auto& m : g_marks) g_free.push_back(m);
+        g_marks.clear();
+        g_launches.store(0);
+    }
+    return DFLOP_OK;
+}

@@ -1,0 +1,318 @@
+"""GPU parity: the CUDA path through the C-ABI (libdflop.so) against the CPU oracle on the
+same seeded inputs.  Tolerances: predict fp32 vs fp64 <= 1e-5 relative
+(north_star); ticks |q_gpu - q_orc| <= 1 + 1e-5 q; everything downstream of the shared
+integer costs bit-exact.  -m gpu.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_25120_b200 import synth  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def D():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2603_25120_b200 import dflop
+    dflop.lib()
+    return dflop
+
+
+def dev_u32(a):
+    return torch.from_numpy(np.ascontiguousarray(a).astype(np.uint32).view(np.int32)).cuda()
+
+
+def host_u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def host_u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def feats(p, b=0):
+    t, f, x = p.features(b)
+    return (t, f, x), (dev_u32(t), dev_u32(f), dev_u32(x))
+
+
+PLAN4 = dict(e_tp=8, e_pp=2, e_dp=1, l_tp=8, l_pp=6, l_dp=1, n_mb=64)
+
+
+def plan_of(p):
+    return p.plan if p.plan is not None else PLAN4
+
+
+# ------------------------------------------------------------------ a1 predict
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_predict_parity(D, O, presets, k):
+    p = presets[k]
+    pl = plan_of(p)
+    for b in (0, 1):
+        (t, f, x), (dt, df, dx) = feats(p, b)
+        cf64, cq, st, _ = O.predict(p.model, pl, t, f, x)
+        assert st == 0
+        f32, ticks = D.predict_costs(p.model, pl, dt, df, dx)
+        g = f32.cpu().numpy().astype(np.float64)
+        ref = cf64 / p.model["tick_ns"]
+        assert np.all((ref == 0) == (g == 0))
+        rel = np.abs(g - ref) / np.maximum(ref, 1e-300)
+        assert rel.max() <= 1e-5, rel.max()
+        q = host_u32(ticks).astype(np.int64)
+        assert np.all(np.abs(q - cq.astype(np.int64)) <= 1 + 1e-5 * cq)
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 5, 4097])
+def test_predict_ragged_sizes(D, O, presets, n):
+    p = presets[5]
+    t, f, x = (a[:n] for a in p.features(3)) if n <= 4096 else (np.tile(a, 2)[:n] for a in p.features(3))
+    cf64, cq, _, _ = O.predict(p.model, p.plan, t, f, x)
+    f32, ticks = D.predict_costs(p.model, p.plan, dev_u32(t), dev_u32(f), dev_u32(x))
+    assert f32.shape == (4, n)
+    if n:
+        g = f32.cpu().numpy().astype(np.float64)
+        ref = cf64 / p.model["tick_ns"]
+        assert (np.abs(g - ref) <= 1e-5 * ref + 1e-30).all()
+
+
+def test_predict_overflow_status(D, presets):
+    p = presets[5]
+    m = dict(p.model)
+    m["tick_ns"] = 1e-3   # every second-scale cost overflows 2^32 ticks
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    (_, _, _), (dt, df, dx) = feats(p)
+    _, ticks = D.predict_costs(m, p.plan, dt, df, dx, dev_status=st)
+    assert int(st.item()) & D.DEV_COST_OVERFLOW
+    assert (host_u32(ticks) == 0xFFFFFFFF).any()
+
+
+# ------------------------------------------------------------------ a4 simulate
+def test_simulate_parity(D, O):
+    rng = np.random.default_rng(5)
+    for S, M in [(1, 1), (1, 7), (2, 1), (4, 6), (8, 32), (16, 64), (32, 3), (5, 129)]:
+        Cn = 24
+        fwd, bwd = synth.random_durations(Cn, S, M, seed=S * 1000 + M, hi=int(rng.integers(1, 1000)))
+        ms, busy = D.simulate_1f1b(torch.from_numpy(fwd.view(np.int64)).cuda(),
+                                   torch.from_numpy(bwd.view(np.int64)).cuda())
+        ms, busy = host_u64(ms), host_u64(busy)
+        for c in range(Cn):
+            T, b = O.simulate_1f1b(fwd[c], bwd[c])
+            assert ms[c] == T and (busy[c] == b).all(), (S, M, c)
+
+
+def test_simulate_uniform_closed_form(D):
+    for S in (1, 3, 8, 16, 32):
+        for M in (1, 5, 33):
+            fwd = np.full((2, S, M), 3, np.uint64)
+            bwd = np.full((2, S, M), 7, np.uint64)
+            ms, _ = D.simulate_1f1b(torch.from_numpy(fwd.view(np.int64)).cuda(),
+                                    torch.from_numpy(bwd.view(np.int64)).cuda())
+            assert (host_u64(ms) == (M + S - 1) * 10).all()
+
+
+def test_simulate_shape_errors(D):
+    z = torch.zeros((1, 33, 2), dtype=torch.int64, device="cuda")
+    with pytest.raises(D.DflopError) as e:
+        D.simulate_1f1b(z, z)
+    assert e.value.code == 2
+
+
+# ------------------------------------------------------------------ a2-a5 balance
+def gpu_balance(D, q_dev, plan, K, R, G, seed, c0, c1, mode=0):
+    r = D.balance_microbatches(q_dev, plan, K, R, G, seed, c0, c1, mode=mode, want_groups=True, per_candidate=True)
+    best = D.cand_result(r["best"])
+    return dict(best=best, assign=host_u32(r["assign"]), offsets=host_u32(r["offsets"]),
+                items=host_u32(r["items"])[: q_dev.shape[1]], cT=host_u64(r["cand_T"]), cC=host_u64(r["cand_cmax"]))
+
+
+def check_balance(D, O, q_host, plan, K, R, G, seed, c0, c1, mode=0, threads=None):
+    q_dev = dev_u32(q_host)
+    g = gpu_balance(D, q_dev, plan, K, R, G, seed, c0, c1, mode)
+    o = O.balance_threaded(q_host, plan, K, R, G, seed, c0, c1, mode=mode, threads=threads)
+    assert (g["cT"] == o["cand_T"]).all(), np.nonzero(g["cT"] != o["cand_T"])[0][:10]
+    assert (g["cC"] == o["cand_cmax"]).all()
+    assert g["best"]["cand"] == o["c"] and g["best"]["makespan"] == o["T"] and g["best"]["cmax"] == o["cmax"]
+    assert (g["assign"] == o["assign"]).all()
+    m = plan["n_mb"] * plan["l_dp"]
+    off, items = O.groups(o["assign"], m)
+    assert (g["offsets"] == off).all() and (g["items"] == items).all()
+    assert g["best"]["key"] == (o["T"] << 24) | o["c"]
+    return g, o
+
+
+@pytest.mark.parametrize("k,c0,c1", [(1, 0, 4096), (2, 0, 2048), (3, 0, 512), (5, 0, 48)])
+def test_balance_parity_presets(D, O, presets, k, c0, c1):
+    p = presets[k]
+    pl = plan_of(p)
+    (t, f, x), (dt, df, dx) = feats(p)
+    _, ticks = D.predict_costs(p.model, pl, dt, df, dx, want_f32=False)
+    q_gpu = host_u32(ticks)
+    # shared integer array, direction 1: the GPU's integers fed to the oracle
+    check_balance(D, O, q_gpu, pl, p.K, p.R, p.G, p.seed(0), c0, c1)
+    # direction 2: the oracle's integers uploaded to the GPU
+    _, q_orc, _, _ = O.predict(p.model, pl, t, f, x)
+    check_balance(D, O, q_orc, pl, p.K, p.R, p.G, p.seed(0), c0, min(c1, c0 + 64))
+
+
+def test_balance_shard_window_config5(D, O, presets):
+    p = presets[5]
+    _, q, _, _ = O.predict(p.model, p.plan, *p.features(2))
+    check_balance(D, O, q, p.plan, p.K, p.R, p.G, p.seed(2), 777_000, 777_024)
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=0, plan=dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=2, l_dp=1, n_mb=3)),
+    dict(n=1, plan=dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=1, l_dp=1, n_mb=1)),
+    dict(n=5, plan=dict(e_tp=1, e_pp=2, e_dp=1, l_tp=1, l_pp=1, l_dp=2, n_mb=4)),        # n < m
+    dict(n=37, plan=dict(e_tp=1, e_pp=3, e_dp=2, l_tp=1, l_pp=5, l_dp=3, n_mb=5)),       # replicas
+    dict(n=700, plan=dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=7, l_dp=2, n_mb=150)),    # wide apos m > 255
+    dict(n=300, plan=dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=1, l_dp=1, n_mb=2)),      # list overflow path
+    dict(n=129, plan=dict(e_tp=1, e_pp=16, e_dp=1, l_tp=1, l_pp=16, l_dp=1, n_mb=9)),    # S = 32
+])
+def test_balance_edge_cases(D, O, case):
+    n, plan = case["n"], case["plan"]
+    q = synth.random_costs(n, seed=n + 17, hi=5000, heavy=True)
+    for G in (1, 8, 16):
+        check_balance(D, O, q, plan, K=300, R=6, G=G, seed=(n, 3), c0=0, c1=40)
+
+
+def test_balance_64bit_path(D, O, presets):
+    # 1 ns ticks: config 2's bucket sums exceed 2^32 -> 64-bit candidate kernel
+    p = presets[2]
+    m = dict(p.model)
+    m["tick_ns"] = 1.0
+    _, q, st, _ = O.predict(m, p.plan, *p.features(0))
+    assert st == 0 and int(q[2].astype(np.int64).sum() + q[3].sum()) >= 2 ** 32
+    check_balance(D, O, q, p.plan, p.K, p.R, p.G, p.seed(0), 0, 256)
+
+
+def test_balance_exhaustive_vs_oracle_and_bruteforce(D, O):
+    import bruteforce as BF
+    rng = np.random.default_rng(21)
+    for trial in range(6):
+        n = int(rng.integers(2, 8))
+        plan = dict(e_tp=1, e_pp=int(rng.integers(1, 3)), e_dp=1, l_tp=1, l_pp=int(rng.integers(1, 3)),
+                    l_dp=int(rng.integers(1, 3)), n_mb=int(rng.integers(1, 3)))
+        m = plan["n_mb"] * plan["l_dp"]
+        K = m ** n
+        q = rng.integers(0, 50, (4, n)).astype(np.uint32)
+        g, o = check_balance(D, O, q, plan, K, 0, 1, (0, 0), 0, K, mode=1)
+        bf = list(BF.all_assignments(q.tolist(), plan))
+        assert g["best"]["makespan"] == min(b[2] for b in bf)
+
+
+def test_balance_sharding_independent_of_g(D, O, presets):
+    # the winner of the family does not depend on how [0, K) is split
+    p = presets[3]
+    _, q, _, _ = O.predict(p.model, p.plan, *p.features(0))
+    qd = dev_u32(q)
+    K = 1024
+    whole = D.cand_result(D.balance_microbatches(qd, p.plan, K, p.R, p.G, p.seed(0), 0, K)["best"])
+    for Gs in (2, 3, 8):
+        keys = []
+        for g in range(Gs):
+            b, e = K * g // Gs, K * (g + 1) // Gs
+            keys.append(D.cand_result(D.balance_microbatches(qd, p.plan, K, p.R, p.G, p.seed(0), b, e)["best"])["key"])
+        assert min(keys) == whole["key"]
+
+
+def test_balance_argument_errors(D, presets):
+    p = presets[1]
+    q = dev_u32(np.zeros((4, 8), np.uint32))
+    with pytest.raises(D.DflopError) as e:
+        D.balance_microbatches(q, p.plan, 0, 1, 1, (0, 0))
+    assert e.value.code == 1
+    with pytest.raises(D.DflopError):
+        D.balance_microbatches(q, p.plan, 10, 1, 17, (0, 0))
+    with pytest.raises(D.DflopError):
+        D.balance_microbatches(q, dict(p.plan, n_mb=70000), 10, 1, 1, (0, 0))
+    with pytest.raises(D.DflopError):
+        D.balance_microbatches(q, p.plan, 10, 1, 1, (0, 0), mode=1)   # 4^8 > 10
+
+
+# ------------------------------------------------------------------ full-size, bench launch config
+def test_config5_full_family_sampled(D, O, presets):
+    """K = 10^6 at N = 4096 (the bench's launch configuration): sampled candidates checked one
+    by one against the oracle, the winner re-derived from the per-candidate array."""
+    p = presets[5]
+    (t, f, x), (dt, df, dx) = feats(p, 0)
+    _, ticks = D.predict_costs(p.model, p.plan, dt, df, dx, want_f32=False)
+    r = D.balance_microbatches(ticks, p.plan, p.K, p.R, p.G, p.seed(0), per_candidate=True)
+    best = D.cand_result(r["best"])
+    cT, cC = host_u64(r["cand_T"]), host_u64(r["cand_cmax"])
+    c_star = int(np.lexsort((np.arange(p.K), cT))[0])
+    assert best["cand"] == c_star and best["makespan"] == cT[c_star] and best["cmax"] == cC[c_star]
+    q = host_u32(ticks)
+    rng = np.random.default_rng(99)
+    sample = sorted(set([0, 1, 2, p.K - 1, c_star] + rng.integers(0, p.K, 24).tolist()))
+    pi = O.base_order(q)
+    for c in sample:
+        a, T, cm = O.run_candidate(q, p.plan, p.K, p.R, p.G, p.seed(0), c, order=pi)
+        assert (T, cm) == (int(cT[c]), int(cC[c])), c
+        if c == c_star:
+            assert (host_u32(r["assign"]) == a).all()
+
+
+# ------------------------------------------------------------------ a6 search
+def test_search_fixed_equals_balance(D, O, presets):
+    p = presets[2]
+    (t, f, x), (dt, df, dx) = feats(p)
+    res = D.search_plans(p.model, dt, df, dx, K=2048, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan)
+    _, q, _, _ = O.predict(p.model, p.plan, t, f, x)
+    _, ticks = D.predict_costs(p.model, p.plan, dt, df, dx, want_f32=False)
+    o = O.balance_threaded(host_u32(ticks), p.plan, 2048, p.R, p.G, p.seed(0), per_candidate=False)
+    assert res["makespan"] == o["T"] and res["cand"] == o["c"] and res["cmax"] == o["cmax"]
+    assert (host_u32(res["assign"]) == o["assign"]).all()
+
+
+def test_search_alg1_stage_a_and_b(D, O, presets):
+    p = presets[4]
+    (t, f, x), (dt, df, dx) = feats(p)
+    cl = p.cluster
+    n_cfg = len(O.enumerate_configs(cl["n_gpus"], cl["gpus_per_node"]))
+    sa = torch.empty(6_541_832, dtype=torch.int64, device="cuda")
+    K, P = 8, 4
+    res = D.search_plans(p.model, dt, df, dx, K=K, R=p.R, G=p.G, seed=p.seed(0), cluster=cl, mem=p.mem(),
+                         gbs=p.gbs, top_p=P, stage_a_out=sa)
+    assert res["n_configs"] == n_cfg == 7194 and res["n_pairs"] == 6_541_832
+    mb, ms = O.batch_means(p.model, t, f, x)
+    T_orc, cfgs = O.stage_a_all(p.model, p.mem(), cl["n_gpus"], cl["gpus_per_node"], p.gbs, mb, ms)
+    T_gpu = host_u64(sa)
+    # fp64 with identical, FMA-free operation order on both sides: expected bit-identical
+    assert (T_gpu == T_orc).all(), np.count_nonzero(T_gpu != T_orc)
+    assert res["n_feasible"] == int(np.count_nonzero(T_orc != np.uint64(2 ** 64 - 1)))
+    top = O.stage_a_top(T_orc, P)
+    e, i = O.pair_to_config(cfgs, p.gbs, top[0])
+    c = cfgs[e]
+    assert res["alg1_plan"] == dict(e_tp=int(c[0]), e_pp=int(c[1]), e_dp=int(c[2]), l_tp=int(c[3]), l_pp=int(c[4]),
+                                    l_dp=int(c[5]), n_mb=i)
+    # Stage B: the oracle balances the same P plans on the GPU's integer costs
+    best = None
+    for rank, pidx in enumerate(top):
+        e, i = O.pair_to_config(cfgs, p.gbs, pidx)
+        c = cfgs[e]
+        pl = dict(e_tp=int(c[0]), e_pp=int(c[1]), e_dp=int(c[2]), l_tp=int(c[3]), l_pp=int(c[4]), l_dp=int(c[5]),
+                  n_mb=i)
+        _, ticks = D.predict_costs(p.model, pl, dt, df, dx, want_f32=False)
+        o = O.balance_threaded(host_u32(ticks), pl, K, p.R, p.G, p.seed(0), per_candidate=False)
+        key = (o["T"], rank, o["c"])
+        if best is None or key < best[0]:
+            best = (key, pl, o)
+    (T, rank, cstar), pl, o = best
+    assert res["makespan"] == T and res["stage_a_rank"] == rank and res["cand"] == cstar
+    assert res["plan"] == pl and res["cmax"] == o["cmax"]
+    assert (host_u32(res["assign"]) == o["assign"]).all()
+
+
+def test_search_infeasible(D, presets):
+    p = presets[4]
+    (_, _, _), (dt, df, dx) = feats(p)
+    mem = p.mem()
+    mem["mem_per_gpu"] = 1.0
+    with pytest.raises(D.DflopError) as e:
+        D.search_plans(p.model, dt, df, dx, K=4, R=1, G=8, seed=(1, 1), cluster=p.cluster, mem=mem, gbs=p.gbs,
+                       top_p=2)
+    assert e.value.code == 4
