@@ -449,18 +449,20 @@ struct SearchLayout {
     size_t bal_bytes;
 };
 
-static size_t balance_bound(uint32_t n, uint32_t m_max, int device) {
-    cudaDeviceProp prop;
-    cudaGetDeviceProperties(&prop, device);
-    const size_t apos_min = std::max<size_t>(16, (n + 15) & ~15u);
-    const size_t slots = (size_t)prop.multiProcessorCount * (prop.sharedMemPerMultiprocessor / apos_min + 1);
+// Upper bound of one balance workspace when the plan is not known yet (Algorithm 1 mode):
+// at most one resident candidate group per candidate of the shard plus one warp of groups
+// per SM, and never more than 1024 groups per SM.
+static size_t balance_bound(uint32_t n, uint32_t m_max, uint32_t K, int device) {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    const size_t slots = std::min<size_t>((size_t)nsm * 1024, (size_t)K + (size_t)nsm * 32);
     const size_t apos_max = std::max<size_t>(16, ((size_t)2 * n + 15) & ~(size_t)15);
     return 256 * 2 + al256((size_t)n * 8) + 2 * al256((size_t)n * 4) + al256((size_t)n * 16) +
-           al256((size_t)n * 32) + 3 * al256(slots * 8) + al256(slots * apos_max) + al256((size_t)m_max * 4) * 2 +
-           4096;
+           al256((size_t)n * 32) + 3 * al256(slots * 8) + al256(slots * 4) + al256(slots * 2 * apos_max) +
+           al256(slots * 4 * (size_t)std::max(1u, n)) + al256((size_t)m_max * 4) * 2 + 4096;
 }
 
-static SearchLayout search_layout(uint32_t n, uint32_t P, uint32_t m_max, uint64_t n_pairs, int device) {
+static SearchLayout search_layout(uint32_t n, uint32_t P, uint64_t n_pairs, size_t bal_bytes, int device) {
     SearchLayout L;
     size_t o = 0;
     L.o_costs = o;   o += al256((size_t)P * 4 * n * 4);
@@ -472,7 +474,7 @@ static SearchLayout search_layout(uint32_t n, uint32_t P, uint32_t m_max, uint64
     L.o_top = o;     o += al256((size_t)P * sizeof(StageATop));
     L.o_feas = o;    o += 256;
     L.o_status = o;  o += 256;
-    L.bal_bytes = balance_bound(n, m_max, device);
+    L.bal_bytes = bal_bytes;
     L.o_bal = o;     o += al256(L.bal_bytes);
     L.total = o;
     return L;
@@ -529,7 +531,20 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
         if ((st = validate_plan(&sp->fixed_plan)) != DFLOP_OK) return st;
         m_max = sp->fixed_plan.n_mb * sp->fixed_plan.l_dp;
     }
-    const SearchLayout L = search_layout(n, P, std::max(1u, m_max), tab ? tab->n_pairs : 0, dev);
+    // balance workspace: exact for a fixed plan, bounded for Algorithm 1 (plans unknown yet)
+    const int G_ = comm ? comm->world : 1, g_ = comm ? comm->rank : 0;
+    uint32_t sb, se;
+    shard(sp->K, g_, G_, &sb, &se);
+    size_t bal_bytes = 0;
+    if (alg1) {
+        bal_bytes = balance_bound(n, std::max(1u, m_max), std::max(1u, se - sb), dev);
+    } else if (se > sb) {
+        BalancePlan bp0;
+        if ((st = plan_balance(n, &sp->fixed_plan, DFLOP_MODE_HEURISTIC, sp->R, sp->G, se - sb, &bp0)) != DFLOP_OK)
+            return st;
+        bal_bytes = bp0.cfg.total;
+    }
+    const SearchLayout L = search_layout(n, P, tab ? tab->n_pairs : 0, bal_bytes, dev);
     if (!ws) {
         *ws_bytes = L.total;
         return DFLOP_OK;

@@ -271,9 +271,9 @@ static int env_int(const char* name, int dflt) {
 
 BalanceConfig balance_config(const BalanceShape& sh, int device) {
     BalanceConfig cfg;
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
-        cfg.why = "cudaGetDeviceProperties failed";
+    const DevAttr prop = dev_attr(device);
+    if (prop.sms == 0) {
+        cfg.why = "cudaDeviceGetAttribute failed";
         return cfg;
     }
     const uint32_t n = sh.n, m = sh.m, S = sh.S;
@@ -291,8 +291,8 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     const bool wide = m > 255;
     cfg.apos_bytes = round16(std::max(16u, n * (wide ? 2u : 1u)));
     const uint32_t scr = round16(std::max(16u + 4u * cfg.cap, (S + 2 * S * sh.D) * 8u));
-    const size_t smem_max = prop.sharedMemPerBlockOptin;
-    const uint32_t nsm = (uint32_t)prop.multiProcessorCount;
+    const size_t smem_max = prop.smem_optin;
+    const uint32_t nsm = (uint32_t)prop.sms;
     const uint32_t per_warp = 32u / (uint32_t)gl;  // candidate groups per warp
     for (int v = 0; v < 3; ++v) {
         const uint32_t asz = v == 2 ? 8u : 4u;
@@ -352,6 +352,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     cfg.o_slot_cmax = o;  o += align256((size_t)cfg.n_slots * 8);
     cfg.o_slot_buf = o;   o += align256((size_t)cfg.n_slots * 4);
     cfg.o_slot_apos = o;  o += align256((size_t)cfg.n_slots * 2 * cfg.apos_bytes);
+    cfg.o_slot_spill = o; o += align256((size_t)cfg.n_slots * 4 * std::max(1u, n));
     cfg.o_grp = o;        o += groups_ws_bytes(n, m);
     cfg.total = o;
     cfg.ok = true;
@@ -372,6 +373,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     u64* slot_cmax = reinterpret_cast<u64*>(ws + cfg.o_slot_cmax);
     uint32_t* slot_buf = reinterpret_cast<uint32_t*>(ws + cfg.o_slot_buf);
     uint8_t* slot_apos = reinterpret_cast<uint8_t*>(ws + cfg.o_slot_apos);
+    uint16_t* slot_spill = reinterpret_cast<uint16_t*>(ws + cfg.o_slot_spill);
     const uint32_t n = a.sh.n;
     const uint32_t allow_pack = a.sh.mode == DFLOP_MODE_EXHAUSTIVE ? 0u : 1u;
 
@@ -389,8 +391,11 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     p.pos_item = order;
     p.item_pos = item_pos;
     p.ops = prog.d_ops;
+    p.levels = prog.d_levels;
+    p.n_levels = prog.n_levels;
     p.hdr = hdr;
     p.slot_apos = slot_apos;
+    p.slot_spill = slot_spill;
     p.slot_key = slot_key;
     p.slot_T = slot_T;
     p.slot_cmax = slot_cmax;
@@ -449,9 +454,8 @@ dflop_status simulate_launch(const uint64_t* fwd, const uint64_t* bwd, uint32_t 
     const size_t per = (size_t)(S + 2 * S * prog.D) * 8;
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceProp prop;
-    cudaGetDeviceProperties(&prop, dev);
-    uint32_t threads = (uint32_t)std::min<size_t>(256, prop.sharedMemPerBlockOptin / per);
+    const DevAttr prop = dev_attr(dev);
+    uint32_t threads = (uint32_t)std::min<size_t>(256, prop.smem_optin / per);
     threads = std::max(1u, std::min(threads, C));
     const size_t dyn = per * threads;
     cudaFuncSetAttribute(reinterpret_cast<const void*>(&k_simulate), cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -21,15 +21,17 @@ struct CandParams {
     const uint32_t* pos_item;    // [n] position -> item index (global)
     const uint32_t* item_pos;    // [n] item index -> position (global)
     const uint32_t* ops;         // 1F1B slot program, n_ops entries
+    const uint32_t* levels;      // n_levels + 1 offsets into ops
     BalanceHeader* hdr;
     uint8_t* slot_apos;          // [n_slots][2][apos_bytes]
+    uint16_t* slot_spill;        // [n_slots][2][n] refinement-list overflow
     u64* slot_key;
     u64* slot_T;
     u64* slot_cmax;
     uint32_t* slot_buf;
     u64* cand_T;                 // optional per-candidate outputs
     u64* cand_cmax;
-    uint32_t n, m, S, e_pp, l_dp, n_mb, R, G, D, n_ops;
+    uint32_t n, m, S, e_pp, l_dp, n_mb, R, G, D, n_ops, n_levels;
     uint32_t c_begin, c_end, id_base, seed0, seed1;
     uint32_t exhaustive, wide, cap, apos_bytes, want_variant;
     uint32_t tbl_bytes, cand_bytes, off_fl, off_scr;

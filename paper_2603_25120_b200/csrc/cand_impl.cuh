@@ -120,6 +120,64 @@ DFLOP_DEV uint64_t make_perm(uint32_t g, uint32_t c, uint32_t ng, uint32_t k0, u
     return perm;
 }
 
+// Warp-cooperative group permutations.  The 32/GL candidate groups of a warp walk the same
+// base-order groups in lockstep, so the Philox calls of W consecutive groups of all of them
+// (32/GL x W x nc calls, nc = ceil((G-1)/4)) are spread over the 32 lanes (<= 4 calls each),
+// the words are exchanged with shuffles and lane u = cg*W + gg runs the Fisher-Yates of
+// candidate group cg, base group g0 + gg.  Same words, same swaps as make_perm.
+template <int GL>
+DFLOP_DEV uint64_t batch_perms(uint32_t g0, uint32_t W, uint32_t nc, uint32_t c, uint32_t n, uint32_t G, uint32_t k0,
+                               uint32_t k1) {
+    constexpr uint32_t cw = 32u / GL;  // candidate groups per warp
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t per_cg = W * nc, tasks = cw * per_cg;
+    uint32_t w[4][4];
+#pragma unroll
+    for (uint32_t k = 0; k < 4; ++k) {
+        const uint32_t t = lane + 32u * k;
+        const uint32_t cg = min(t / per_cg, cw - 1u);
+        const uint32_t cc = __shfl_sync(FULL, c, cg * GL);
+        w[k][0] = w[k][1] = w[k][2] = w[k][3] = 0u;
+        if (t < tasks) {
+            const uint32_t rem = t % per_cg, gg = rem / nc, pc = rem % nc;
+            const Philox4 r = philox4x32_10(g0 + gg, cc, 0u, pc, k0, k1);
+            w[k][0] = r.x;
+            w[k][1] = r.y;
+            w[k][2] = r.z;
+            w[k][3] = r.w;
+        }
+        if (32u * (k + 1) >= tasks) break;  // warp-uniform
+    }
+    const uint32_t cg = min(lane / W, cw - 1u), gg = lane % W;
+    const uint32_t cc = __shfl_sync(FULL, c, cg * GL);
+    const uint32_t start = (g0 + gg) * G;
+    const uint32_t ng = start < n ? min(G, n - start) : 0u;
+    uint64_t perm = 0xFEDCBA9876543210ull;
+    for (uint32_t pc = 0; pc < nc; ++pc) {
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+            const uint32_t t = (cg * W + gg) * nc + pc;
+            uint32_t word = 0;
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) {
+                const uint32_t v = __shfl_sync(FULL, w[k][q], t & 31u);
+                if ((t >> 5) == k) word = v;
+                if (32u * (k + 1) >= tasks) break;  // warp-uniform
+            }
+            const uint32_t idx = pc * 4 + q;
+            if (idx + 1 < ng) {
+                const uint32_t tt = ng - 1 - idx;
+                const uint32_t r = mulhi32(word, tt + 1);
+                const uint64_t a = (perm >> (4 * tt)) & 15ull, b = (perm >> (4 * r)) & 15ull;
+                const uint64_t x = a ^ b;
+                perm ^= (x << (4 * tt)) | (x << (4 * r));
+            }
+        }
+    }
+    if (cc < 2 || lane >= cw * W) perm = 0xFEDCBA9876543210ull;
+    return perm;
+}
+
 // ---------------------------------------------------------------- item table access
 template <typename A, bool SM>
 struct Tbl {
@@ -158,7 +216,9 @@ DFLOP_DEV void set_apos(uint8_t* apos, uint32_t pos, uint32_t j, bool wide) {
 }
 
 // Processes one 16-byte block of the assignment (16 positions u8 / 8 positions u16) and calls
-// f(pos, which) for every position assigned to ja (which = 0) or jb (which = 1).
+// f(pos, which) for every position assigned to ja (which = 0) or jb (which = 1).  A word
+// is inspected byte by byte only when the zero-byte test of (word ^ target) fires, which is
+// exact as a predicate: (x - 0x01..01) & ~x & 0x80..80 != 0 iff some byte of x is zero.
 template <typename F>
 DFLOP_DEV void scan_words(const uint4 v, uint32_t blk, bool wide, uint32_t ja, uint32_t jb, F&& f) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -166,26 +226,30 @@ DFLOP_DEV void scan_words(const uint4 v, uint32_t blk, bool wide, uint32_t ja, u
         const uint32_t A4 = ja * 0x01010101u, B4 = jb * 0x01010101u;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            uint32_t ea = __vcmpeq4(w[k], A4), eb = __vcmpeq4(w[k], B4);
-            while (ea | eb) {
-                const uint32_t e = ea ? ea : eb;
-                const int which = ea ? 0 : 1;
-                const int byte = (__ffs(e) - 1) >> 3;
-                f(blk * 16 + 4 * k + byte, which);
-                if (which == 0) ea &= ~(0xFFu << (8 * byte)); else eb &= ~(0xFFu << (8 * byte));
+            const uint32_t x = w[k] ^ A4, y = w[k] ^ B4;
+            const uint32_t h = ((x - 0x01010101u) & ~x) | ((y - 0x01010101u) & ~y);
+            if (h & 0x80808080u) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t val = (w[k] >> (8 * b)) & 0xFFu;
+                    if (val == ja) f(blk * 16 + 4 * k + b, 0);
+                    else if (val == jb) f(blk * 16 + 4 * k + b, 1);
+                }
             }
         }
     } else {
         const uint32_t A2 = ja * 0x00010001u, B2 = jb * 0x00010001u;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            uint32_t ea = __vcmpeq2(w[k], A2), eb = __vcmpeq2(w[k], B2);
-            while (ea | eb) {
-                const uint32_t e = ea ? ea : eb;
-                const int which = ea ? 0 : 1;
-                const int half = (__ffs(e) - 1) >> 4;
-                f(blk * 8 + 2 * k + half, which);
-                if (which == 0) ea &= ~(0xFFFFu << (16 * half)); else eb &= ~(0xFFFFu << (16 * half));
+            const uint32_t x = w[k] ^ A2, y = w[k] ^ B2;
+            const uint32_t h = ((x - 0x00010001u) & ~x) | ((y - 0x00010001u) & ~y);
+            if (h & 0x80008000u) {
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const uint32_t val = (w[k] >> (16 * b)) & 0xFFFFu;
+                    if (val == ja) f(blk * 8 + 2 * k + b, 0);
+                    else if (val == jb) f(blk * 8 + 2 * k + b, 1);
+                }
             }
         }
     }
@@ -206,10 +270,16 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
     const bool wide = p.wide != 0;
     const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
     const uint32_t jmask = (1u << sh) - 1u;
-    uint32_t g = 0;
-    for (uint32_t start = 0; start < n; start += G, ++g) {
+    const uint32_t nc = (G - 1 + 3) / 4;  // Philox calls per group
+    const uint32_t W = nc ? max(1u, 32u / ((32u / GL) * nc)) : 1u;
+    const uint32_t lane = threadIdx.x & 31u, mycg = lane / GL;
+    const uint32_t n_groups = (n + G - 1) / G;
+    for (uint32_t g0 = 0; g0 < n_groups; g0 += W) {
+      const uint64_t preg = nc ? batch_perms<GL>(g0, W, nc, c, n, G, p.seed0, p.seed1) : 0xFEDCBA9876543210ull;
+      for (uint32_t gg = 0; gg < W && g0 + gg < n_groups; ++gg) {
+        const uint32_t start = (g0 + gg) * G;
         const uint32_t ng = min(G, n - start);
-        const uint64_t perm = (c >= 2 && ng > 1) ? make_perm(g, c, ng, p.seed0, p.seed1) : 0xFEDCBA9876543210ull;
+        const uint64_t perm = nc ? __shfl_sync(FULL, preg, mycg * W + gg) : 0xFEDCBA9876543210ull;
         for (uint32_t t = 0; t < ng; ++t) {
             const uint32_t pos = start + (uint32_t)((perm >> (4 * t)) & 15ull);
             const ItemRec<A> it = T.item(pos);
@@ -260,6 +330,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
             }
             __syncwarp(FULL);
         }
+      }
     }
 }
 
@@ -268,13 +339,15 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
 // group of a warp issues the same shuffle sequence.
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
-                      uint8_t* apos, uint8_t* scr, uint32_t gl, bool apply) {
+                      uint8_t* apos, uint8_t* scr, uint16_t* spill, uint32_t gl, bool apply) {
     const uint32_t m = p.m, cap = p.cap;
     const bool wide = p.wide != 0;
     const uint32_t nblk = p.apos_bytes / 16;
     uint32_t* cnt = reinterpret_cast<uint32_t*>(scr);
     uint16_t* ls = reinterpret_cast<uint16_t*>(scr + 16);
     uint16_t* lp = ls + cap;
+    uint16_t* gss = spill;           // global spill of ls
+    uint16_t* gsp = spill + p.n;     // global spill of lp
     for (uint32_t r = 0; r < p.R; ++r) {
         // bottleneck bucket j* = lowest j with maximal W_j = max(E_j, L_j)
         A Wb = 0;
@@ -300,7 +373,8 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             cnt[1] = 0;
         }
         __syncwarp(FULL);
-        // member lists of j* (ls) and j' (lp): 16-byte L2 scans of the assignment, 4 in flight
+        // member lists of j* (ls) and j' (lp): 16-byte L2 scans of the assignment, 4 in flight;
+        // entries past the shared-memory capacity spill to the slot's global area
         for (uint32_t b0 = gl; b0 < nblk; b0 += 4 * GL) {
             uint4 v[4];
 #pragma unroll
@@ -312,7 +386,10 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             for (int u = 0; u < 4; ++u)
                 scan_words(v[u], b0 + u * GL, wide, js, jp, [&](uint32_t pos, int which) {
                     const uint32_t at = atomicAdd(&cnt[which], 1u);
-                    if (at < cap) (which ? lp : ls)[at] = (uint16_t)pos;
+                    if (at < cap)
+                        (which ? lp : ls)[at] = (uint16_t)pos;
+                    else
+                        (which ? gsp : gss)[at - cap] = (uint16_t)pos;
                 });
         }
         __syncwarp(FULL);
@@ -321,17 +398,15 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         A bsc = amax<A>();
         uint32_t bi = 0xFFFFFFFFu, brk = 0xFFFFFFFFu;
         u64 bkey = ~0ull;  // 32-bit scores: (score << 32 | item << 16 | rank), a branch-free min
+        const uint32_t nBs = min(nB, cap);
         // all (i, i') with i in j*, i' in {NONE} u j'; lexicographic min of (score, i, rank(i'))
-        auto eval_i = [&](uint32_t pi) {
+        for (uint32_t u = gl; u < nA; u += GL) {
+            const uint32_t pi = u < cap ? (uint32_t)ls[u] : (uint32_t)__ldcg(gss + (u - cap));
             const Pair2<A> a = T.el(pi);
             const uint32_t ii = T.idx(pi);
             const A se = Bs.a - a.a, sl = Bs.b - a.b;  // j* without i
             const A pe = Bp.a + a.a, pl = Bp.b + a.b;  // j' with i
             const A s0 = maxa(maxa(se, sl), maxa(pe, pl));
-            if (sizeof(A) == 4)
-                bkey = min(bkey, ((u64)s0 << 32) | ((u64)ii << 16));
-            else
-                lex_update(bsc, bi, brk, s0, ii, 0u);
             auto pair = [&](uint32_t pj) {
                 const Pair2<A> b = T.el(pj);
                 const uint32_t rk = T.idx(pj) + 1u;
@@ -342,22 +417,20 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 else
                     lex_update(bsc, bi, brk, maxa(s1, s2), ii, rk);
             };
-            if (nB <= cap) {
-                for (uint32_t v = 0; v < nB; ++v) pair(lp[v]);
-            } else {
-                for (uint32_t bb = 0; bb < nblk; ++bb)
-                    scan_block(apos, bb, wide, jp, jp, [&](uint32_t pos, int which) {
-                        if (which == 0) pair(pos);
-                    });
+            if (sizeof(A) == 4)
+                bkey = min(bkey, ((u64)s0 << 32) | ((u64)ii << 16));
+            else
+                lex_update(bsc, bi, brk, s0, ii, 0u);
+            uint32_t v = 0;
+            for (; v + 4 <= nBs; v += 4) {
+                const uint32_t q0 = lp[v], q1 = lp[v + 1], q2 = lp[v + 2], q3 = lp[v + 3];
+                pair(q0);
+                pair(q1);
+                pair(q2);
+                pair(q3);
             }
-        };
-        if (nA <= cap) {
-            for (uint32_t u = gl; u < nA; u += GL) eval_i(ls[u]);
-        } else {
-            for (uint32_t b = gl; b < nblk; b += GL)
-                scan_block(apos, b, wide, js, js, [&](uint32_t pos, int which) {
-                    if (which == 0) eval_i(pos);
-                });
+            for (; v < nBs; ++v) pair(lp[v]);
+            for (v = cap; v < nB; ++v) pair(__ldcg(gsp + (v - cap)));
         }
         if (sizeof(A) == 4) {
 #pragma unroll
@@ -397,46 +470,61 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
 
 // ---------------------------------------------------------------- 1F1B score (O7)
 // Replica rho runs buckets j = k*L_dp + rho as slots k (R10); stages < E_pp take (EF, E-EF),
-// the rest (LF, L-LF) (R7).  Ops in the host-built topological order, rings of depth D.
-template <typename A, bool PK>
-DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr) {
+// the rest (LF, L-LF) (R7).  The host-built topological order is grouped in Kahn levels;
+// the GL lanes of the group run the ops of one level concurrently (distinct stages), rings
+// of depth D carry the end times between stages.
+template <typename A, bool PK, int GL>
+DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr,
+                         uint32_t gl) {
     const uint32_t S = p.S, D = p.D, Dm = p.D - 1;
     u64* last = scr;
     u64* FR = scr + S;
     u64* BR = FR + S * D;
     u64 T = 0;
     for (uint32_t rho = 0; rho < p.l_dp; ++rho) {
-        for (uint32_t s = 0; s < S; ++s) last[s] = 0;
-        for (uint32_t q = 0; q < p.n_ops; ++q) {
-            const uint32_t op = __ldg(p.ops + q);
-            const uint32_t kind = op_kind(op), s = op_stage(op), k = op_mb(op);
-            const uint32_t j = k * p.l_dp + rho;
-            const Pair2<A> el = EL[j], fl = FL[j];
-            const bool enc = s < p.e_pp;
-            u64 dur, dep = 0;
-            if (kind == 0) {
-                dur = enc ? (u64)fl.a : (u64)fl.b;
-                if (s > 0) dep = FR[(s - 1) * D + (k & Dm)];
-            } else {
-                dur = enc ? (u64)(unpack<A, PK>(el.a, sh) - fl.a) : (u64)(unpack<A, PK>(el.b, sh) - fl.b);
-                dep = (s + 1 < S) ? BR[(s + 1) * D + (k & Dm)] : FR[s * D + (k & Dm)];
+        for (uint32_t s = gl; s < S; s += GL) last[s] = 0;
+        __syncwarp(FULL);
+        uint32_t q0 = __ldg(p.levels);
+        for (uint32_t L = 0; L < p.n_levels; ++L) {
+            const uint32_t q1 = __ldg(p.levels + L + 1);
+            for (uint32_t q = q0 + gl; q < q1; q += GL) {
+                const uint32_t op = __ldg(p.ops + q);
+                const uint32_t kind = op_kind(op), s = op_stage(op), k = op_mb(op);
+                const uint32_t j = k * p.l_dp + rho;
+                const Pair2<A> el = EL[j], fl = FL[j];
+                const bool enc = s < p.e_pp;
+                u64 dur, dep = 0;
+                if (kind == 0) {
+                    dur = enc ? (u64)fl.a : (u64)fl.b;
+                    if (s > 0) dep = FR[(s - 1) * D + (k & Dm)];
+                } else {
+                    dur = enc ? (u64)(unpack<A, PK>(el.a, sh) - fl.a) : (u64)(unpack<A, PK>(el.b, sh) - fl.b);
+                    dep = (s + 1 < S) ? BR[(s + 1) * D + (k & Dm)] : FR[s * D + (k & Dm)];
+                }
+                const u64 l0 = last[s];
+                const u64 end = (l0 > dep ? l0 : dep) + dur;
+                last[s] = end;
+                if (kind == 0)
+                    FR[s * D + (k & Dm)] = end;
+                else
+                    BR[s * D + (k & Dm)] = end;
             }
-            const u64 l0 = last[s];
-            const u64 end = (l0 > dep ? l0 : dep) + dur;
-            last[s] = end;
-            if (kind == 0)
-                FR[s * D + (k & Dm)] = end;
-            else
-                BR[s * D + (k & Dm)] = end;
+            q0 = q1;
+            __syncwarp(FULL);
         }
-        for (uint32_t s = 0; s < S; ++s) T = last[s] > T ? last[s] : T;
+        u64 t = 0;
+        for (uint32_t s = gl; s < S; s += GL) t = last[s] > t ? last[s] : t;
+        t = max_reduce<u64, GL>(t, FULL);
+        T = t > T ? t : T;
+        __syncwarp(FULL);
     }
     return T;
 }
 
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
-                             Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint32_t gl, u64& Tc, u64& cmax) {
+                             Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* spill, uint32_t gl, u64& Tc,
+                             u64& cmax) {
     const uint32_t m = p.m;
     for (uint32_t j = gl; j < m; j += GL) {
         EL[j] = PK ? Pair2<A>{(A)j, (A)j} : Pair2<A>{0, 0};
@@ -462,7 +550,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         __syncwarp(FULL);
     } else {
         lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, gl);
-        if (m >= 2) refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, gl, c >= 2);
+        if (m >= 2) refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, spill, gl, c >= 2);
     }
     A cm = 0;
     for (uint32_t j = gl; j < m; j += GL) {
@@ -470,8 +558,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         cm = maxa(cm, unpack<A, PK>(maxa(el.a, el.b), sh));
     }
     cmax = (u64)max_reduce<A, GL>(cm, FULL);
-    Tc = (gl == 0) ? score_1f1b<A, PK>(p, sh, EL, FL, reinterpret_cast<u64*>(scr)) : 0;
-    __syncwarp(FULL);
+    Tc = score_1f1b<A, PK, GL>(p, sh, EL, FL, reinterpret_cast<u64*>(scr), gl);
 }
 
 template <typename A, bool PK, int GL, bool SM>
@@ -503,6 +590,7 @@ __global__ void __launch_bounds__(1024) k_candidates(CandParams p) {
     uint8_t* scr = base + p.off_scr;
     const uint32_t slot = blockIdx.x * cpb + grp;
     uint8_t* bufs = p.slot_apos + (size_t)slot * 2 * p.apos_bytes;
+    uint16_t* spill = p.slot_spill + (size_t)slot * 2 * p.n;
     // padding past n never matches a bucket (0xFF / 0xFFFF)
     const uint32_t used = p.n * (p.wide ? 2u : 1u);
     for (uint32_t b = used + gl; b < p.apos_bytes; b += GL) {
@@ -517,7 +605,7 @@ __global__ void __launch_bounds__(1024) k_candidates(CandParams p) {
         const uint32_t c = valid ? c0 + grp : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
         u64 Tc, cmax;
-        run_candidate<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, gl, Tc, cmax);
+        run_candidate<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, spill, gl, Tc, cmax);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
         u64 key;
         if (Tc >= (1ull << 40)) {

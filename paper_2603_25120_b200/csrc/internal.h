@@ -13,6 +13,14 @@ namespace dflop {
 
 void set_error(const char* fmt, ...);
 
+// cached device attributes (cudaGetDeviceProperties is slow; attributes are queried once)
+struct DevAttr {
+    int sms;
+    size_t smem_optin;     // max dynamic shared memory per block (opt-in)
+    size_t smem_per_sm;
+};
+DevAttr dev_attr(int device);
+
 // instrumentation (profile.cpp)
 void count_launches(uint32_t k);
 bool profiling();
@@ -38,8 +46,9 @@ cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* const
 // ---------------------------------------------------------------- 1F1B slot program
 struct SlotProgram {
     uint32_t S = 0, M = 0, D = 0;  // D = ring depth (power of two)
-    const uint32_t* d_ops = nullptr;  // device copy, 2*S*M entries
-    uint32_t n_ops = 0;
+    const uint32_t* d_ops = nullptr;     // device copy, 2*S*M entries
+    const uint32_t* d_levels = nullptr;  // device, n_levels + 1 offsets into d_ops
+    uint32_t n_ops = 0, n_levels = 0;
 };
 // Builds (once per (S, M) and device) a topological order of the 1F1B DAG by Kahn levels.
 dflop_status get_slot_program(uint32_t S, uint32_t M, SlotProgram* out);
@@ -66,7 +75,7 @@ struct BalanceConfig {
     uint32_t n_slots = 0;
     // workspace layout (byte offsets)
     size_t o_hdr, o_keys, o_order, o_item_pos, o_items32, o_items64, o_slot_key, o_slot_T, o_slot_cmax,
-        o_slot_buf, o_slot_apos, o_grp, total;
+        o_slot_buf, o_slot_apos, o_slot_spill, o_grp, total;
     bool ok = false;
     std::string why;
 };

@@ -44,6 +44,24 @@ void prof_mark(int idx, int which, cudaStream_t s) {  // which = 1..3
     if (idx < (int)g_marks.size()) cudaEventRecord(g_marks[idx].e[which], s);
 }
 
+DevAttr dev_attr(int device) {
+    static std::mutex mu;
+    static std::vector<DevAttr> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)cache.size() <= device) cache.resize(device + 1, DevAttr{0, 0, 0});
+    DevAttr& d = cache[device];
+    if (d.sms == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+        d.sms = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        d.smem_optin = (size_t)v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+        d.smem_per_sm = (size_t)v;
+    }
+    return d;
+}
+
 }  // namespace dflop
 
 using namespace dflop;

@@ -3,7 +3,8 @@
 // that bounds how many produced-but-unconsumed end times a stage must keep.
 //
 // Construction: Kahn's algorithm computes each op's level (longest chain of ops before
-// it); ops are ordered by (level, stage).  Any topological order gives the same longest
+// it); ops are ordered by (level, stage); the level offsets let the lanes of a candidate
+// group evaluate one level in parallel (the ops of a level are on distinct stages).  Any topological order gives the same longest
 // path; this one keeps producer/consumer distances short, so the rings stay shallow.
 // Cached per (device, S, M) in library-owned device memory.
 #include <cuda_runtime.h>
@@ -29,9 +30,10 @@ std::map<std::tuple<int, uint32_t, uint32_t>, Entry> g_cache;
 inline uint32_t enc(uint32_t kind, uint32_t s, uint32_t k) { return (kind << 31) | (s << 16) | k; }
 }  // namespace
 
-static void build_program(uint32_t S, uint32_t M, std::vector<uint32_t>& out, uint32_t& D) {
+static void build_program(uint32_t S, uint32_t M, std::vector<uint32_t>& out, std::vector<uint32_t>& levels,
+                          uint32_t& D) {
     // per-stage op sequences; node id = s * 2M + t
-    const uint32_t L = 2 * M;
+    const uint32_t L_ = 2 * M, L = L_;
     std::vector<uint32_t> kind(S * L), mb(S * L);
     std::vector<uint32_t> posF(S * M), posB(S * M);
     for (uint32_t s = 0; s < S; ++s) {
@@ -86,19 +88,33 @@ static void build_program(uint32_t S, uint32_t M, std::vector<uint32_t>& out, ui
         return a / L < b / L;
     });
     out.resize(N);
-    // ring depth: FIFO distance between production and consumption per edge type
+    // level offsets: ops of one level are on distinct stages and may run concurrently
+    levels.clear();
+    for (uint32_t q = 0; q < N; ++q)
+        if (q == 0 || level[ord[q]] != level[ord[q - 1]]) levels.push_back(q);
+    levels.push_back(N);
+    // ring depth: FIFO distance between production and consumption per edge type.  The ops
+    // of a level run concurrently, so a level's productions are checked against the
+    // consumption state before the level and its consumptions take effect after it.
     std::vector<uint32_t> consF(S, 0), consB(S, 0);
     uint32_t need = 1;
-    for (uint32_t q = 0; q < N; ++q) {
-        const uint32_t v = ord[q], s = v / L, kd = kind[v], k = mb[v];
-        out[q] = enc(kd, s, k);
-        if (kd == 0) {
-            if (s > 0) consF[s - 1] = k + 1;           // consumes F(s-1, k)
-            need = std::max(need, k - consF[s] + 1);   // produces F(s, k)
-        } else {
-            if (s + 1 < S) consB[s + 1] = k + 1;       // consumes B(s+1, k)
-            else consF[s] = k + 1;                     // last stage: consumes its F(k)
-            if (s > 0) need = std::max(need, k - consB[s] + 1);  // B(0, k) is never read
+    for (size_t L = 0; L + 1 < levels.size(); ++L) {
+        for (uint32_t q = levels[L]; q < levels[L + 1]; ++q) {
+            const uint32_t v = ord[q], s = v / L_, kd = kind[v], k = mb[v];
+            out[q] = enc(kd, s, k);
+            if (kd == 0)
+                need = std::max(need, k - consF[s] + 1);                 // produces F(s, k)
+            else if (s > 0)
+                need = std::max(need, k - consB[s] + 1);                 // produces B(s, k); B(0, k) unread
+        }
+        for (uint32_t q = levels[L]; q < levels[L + 1]; ++q) {
+            const uint32_t v = ord[q], s = v / L_, kd = kind[v], k = mb[v];
+            if (kd == 0) {
+                if (s > 0) consF[s - 1] = k + 1;                         // consumes F(s-1, k)
+            } else {
+                if (s + 1 < S) consB[s + 1] = k + 1;                     // consumes B(s+1, k)
+                else consF[s] = k + 1;                                   // last stage: its F(k)
+            }
         }
     }
     D = 1;
@@ -115,23 +131,27 @@ dflop_status get_slot_program(uint32_t S, uint32_t M, SlotProgram* out) {
         *out = it->second.prog;
         return DFLOP_OK;
     }
-    std::vector<uint32_t> ops;
+    std::vector<uint32_t> ops, levels;
     uint32_t D = 1;
-    build_program(S, M, ops, D);
+    build_program(S, M, ops, levels, D);
     if (D > 16) {
         set_error("1F1B ring depth %u > 16 for S=%u M=%u", D, S, M);
         return DFLOP_ERR_UNSUPPORTED;
     }
     Entry e;
-    cudaError_t ce = cudaMalloc(&e.d_ops, ops.size() * sizeof(uint32_t));
+    std::vector<uint32_t> all(ops);
+    all.insert(all.end(), levels.begin(), levels.end());
+    cudaError_t ce = cudaMalloc(&e.d_ops, all.size() * sizeof(uint32_t));
     if (ce != cudaSuccess) return cuda_status(ce, "slot program alloc");
-    ce = cudaMemcpy(e.d_ops, ops.data(), ops.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    ce = cudaMemcpy(e.d_ops, all.data(), all.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
     if (ce != cudaSuccess) return cuda_status(ce, "slot program copy");
     e.prog.S = S;
     e.prog.M = M;
     e.prog.D = D;
     e.prog.d_ops = e.d_ops;
     e.prog.n_ops = (uint32_t)ops.size();
+    e.prog.n_levels = (uint32_t)levels.size() - 1;
+    e.prog.d_levels = e.d_ops + ops.size();
     g_cache[key] = e;
     *out = e.prog;
     return DFLOP_OK;

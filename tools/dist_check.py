@@ -1,0 +1,55 @@
+"""Multi-GPU check of dflop_search_plans (run under torchrun, one rank per GPU).
+
+Every rank evaluates its shard of the candidate family; one NCCL min all-reduce picks the
+winner and its owner broadcasts the assignment.  Rank 0 also runs the whole family on its
+own GPU (comm = NULL) and the two results must be identical (the winner does not depend
+on the number of GPUs).
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 tools/dist_check.py --config 3 --K 8192
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from paper_2603_25120_b200 import dflop as D
+from paper_2603_25120_b200 import sharding, synth
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=3)
+ap.add_argument("--K", type=int, default=8192)
+a = ap.parse_args()
+rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+torch.cuda.set_device(local)
+dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+p = synth.presets()[a.config]
+t, f, x = (torch.from_numpy(v.astype(np.uint32).view(np.int32)).cuda() for v in p.features(0))
+comm = D.Comm(rank, world, local)
+res = D.search_plans(p.model, t, f, x, K=a.K, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan, comm=comm)
+assign = res["assign"].cpu().numpy()
+ok = True
+if rank == 0:
+    ref = D.search_plans(p.model, t, f, x, K=a.K, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan, comm=None)
+    ok = (res["makespan"], res["cand"], res["cmax"]) == (ref["makespan"], ref["cand"], ref["cmax"])
+    ok = ok and bool((assign == ref["assign"].cpu().numpy()).all())
+    ok = ok and res["owner_rank"] == sharding.owner_of(a.K, res["cand"], world)
+# every rank must hold the same winner and assignment
+h = torch.tensor([res["makespan"], res["cand"], int(assign.astype(np.int64).sum())], dtype=torch.int64).cuda()
+hmax, hmin = h.clone(), h.clone()
+dist.all_reduce(hmax, op=dist.ReduceOp.MAX)
+dist.all_reduce(hmin, op=dist.ReduceOp.MIN)
+ok = ok and bool((hmax == hmin).all().item())
+flag = torch.tensor([1 if ok else 0], dtype=torch.int32).cuda()
+dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+if rank == 0:
+    print(json.dumps({"world": world, "config": a.config, "K": a.K, "T": res["makespan"], "cand": res["cand"],
+                      "owner": res["owner_rank"], "ok": bool(flag.item())}), flush=True)
+comm.close()
+dist.destroy_process_group()
+sys.exit(0 if flag.item() else 1)
