@@ -132,22 +132,24 @@ class ClockSampler:
 # ---------------------------------------------------------------- CPU oracle baseline
 def oracle_rate(p, K_family, budget_s, threads=None):
     """The oracle as it stands, on the host cores: predict + candidates over a bounded sample of
-    the same workload.  Returns (candidates/s, sample description, threads used)."""
+    the same workload (consecutive candidate ranges until ~budget_s of wall time).  Returns
+    (candidates/s, sample description, threads used)."""
     from oracle import oracle as O
     threads = threads or os.cpu_count() or 1
     t, f, x = p.features(0)
     t0 = time.perf_counter()
     _, q, st, _ = O.predict(p.model, p.plan, t, f, x)
-    t_pred = time.perf_counter() - t0
-    pilot = threads * 2
-    t0 = time.perf_counter()
-    O.balance_threaded(q, p.plan, K_family, p.R, p.G, p.seed(0), 0, pilot, threads=threads, per_candidate=False)
-    dt = time.perf_counter() - t0
-    n = max(pilot, min(K_family, int(pilot * budget_s / max(dt, 1e-6))))
-    t0 = time.perf_counter()
-    O.balance_threaded(q, p.plan, K_family, p.R, p.G, p.seed(0), 0, n, threads=threads, per_candidate=False)
-    dt = time.perf_counter() - t0 + t_pred
-    return n / dt, f"candidates [0, {n}) of batch 0 (+ predict of all {p.n} samples), {dt:.1f} s", threads
+    done = 0
+    chunk = threads * 8
+    while True:
+        c1 = min(K_family, done + chunk)
+        O.balance_threaded(q, p.plan, K_family, p.R, p.G, p.seed(0), done, c1, threads=threads, per_candidate=False)
+        done = c1
+        dt = time.perf_counter() - t0
+        if dt >= budget_s or done >= K_family:
+            break
+        chunk = min(max(chunk, int(done / dt * 2.0)), threads * 4096)
+    return done / dt, f"candidates [0, {done}) of batch 0 (+ predict of all {p.n} samples), {dt:.1f} s", threads
 
 
 def run_reference(args):

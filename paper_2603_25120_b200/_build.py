@@ -37,11 +37,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), timing: bool = False) -> str:
+    """timing=True builds libdflop_timing.so with -DDFLOP_TIMING (per-phase clock64 counters
+    in the candidate kernel, read with dflop_debug_phase_cycles); a diagnostic build only."""
+    lib = os.path.join(HERE, "libdflop_timing.so") if timing else LIB
+    if timing:
+        extra = tuple(extra) + ("-DDFLOP_TIMING",)
+    if not force and not timing and not _stale():
         return LIB
     inc, libdir = _nccl_dirs()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build_timing" if timing else "build")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + inc, "-I" + os.path.join(ROOT, "include"),
               *ARCH, *extra]
@@ -60,13 +65,13 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
 
     with cf.ThreadPoolExecutor(8) as ex:
         objs = list(ex.map(compile_one, sources()))
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L" + libdir, "-l:libnccl.so.2",
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-L" + libdir, "-l:libnccl.so.2",
            "-Xlinker", "-rpath," + libdir]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timing="--timing" in sys.argv))

@@ -264,6 +264,20 @@ cudaError_t groups_launch(const uint32_t* assign, uint32_t n, uint32_t m, uint32
 }
 
 
+// diagnostic phase counters of the candidate kernel (timing builds only)
+static unsigned long long* phase_counters() {
+#ifdef DFLOP_TIMING
+    static unsigned long long* d = nullptr;
+    if (!d) {
+        cudaMalloc(&d, 8 * sizeof(unsigned long long));
+        cudaMemset(d, 0, 8 * sizeof(unsigned long long));
+    }
+    return d;
+#else
+    return nullptr;
+#endif
+}
+
 static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return (v && *v) ? atoi(v) : dflt;
@@ -311,7 +325,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         // stage the table in shared memory when it leaves room for at least 2 warps of candidates
         cfg.tbl_smem[v] = (size_t)tbl + (size_t)2 * per_warp * cb <= smem_max;
         cfg.tbl_bytes[v] = cfg.tbl_smem[v] ? tbl : 0;
-        uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - cfg.tbl_bytes[v]) / cb, 1024 / gl);
+        uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - cfg.tbl_bytes[v]) / cb, kCandMaxThreads / gl);
         // no more groups than the family needs (one CTA per SM), whole warps only
         cpb = std::min<uint32_t>(cpb, std::max(1u, (sh.n_cand + nsm - 1) / nsm));
         cpb = (cpb + per_warp - 1) / per_warp * per_warp;
@@ -421,6 +435,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     p.wide = a.sh.m > 255;
     p.cap = cfg.cap;
     p.apos_bytes = cfg.apos_bytes;
+    p.phase = phase_counters();
     const int mark = prof_begin(s);
     for (int v = 0; v < 3; ++v) {
         CandParams q = p;
@@ -468,3 +483,15 @@ dflop_status simulate_launch(const uint64_t* fwd, const uint64_t* bwd, uint32_t 
 }
 
 }  // namespace dflop
+
+// Diagnostic: summed clock64 cycles per phase of the candidate kernel (lane 0 of every
+// candidate group), zeros unless built with -DDFLOP_TIMING.  Not part of include/dflop.h.
+extern "C" int dflop_debug_phase_cycles(unsigned long long out[8], int reset) {
+    unsigned long long* d = dflop::phase_counters();
+    for (int k = 0; k < 8; ++k) out[k] = 0;
+    if (!d) return 0;
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, d, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (reset) cudaMemset(d, 0, 8 * sizeof(unsigned long long));
+    return 0;
+}

@@ -10,6 +10,9 @@ namespace dflop {
 //   1  plain 32-bit sums
 //   2  64-bit sums
 constexpr int kVariants = 3;
+// block size cap of the candidate kernel: leaves ~100 registers per thread (64 K per SM);
+// the 1024-thread bound capped the kernel at 64 registers and cost ~10%
+constexpr int kCandMaxThreads = 640;
 
 // Per-launch parameters.  Shared-memory layout (bytes):
 //   [0, tbl_bytes)              CTA item table: ItemRec<A>[n] then u16 pos->item[n]
@@ -35,6 +38,7 @@ struct CandParams {
     uint32_t c_begin, c_end, id_base, seed0, seed1;
     uint32_t exhaustive, wide, cap, apos_bytes, want_variant;
     uint32_t tbl_bytes, cand_bytes, off_fl, off_scr;
+    unsigned long long* phase;   // diagnostic phase counters (timing builds), else null
 };
 
 struct CandLaunch {

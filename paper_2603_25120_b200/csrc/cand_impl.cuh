@@ -41,6 +41,35 @@ DFLOP_DEV A shfl_x(unsigned mask, A v, int off) {
 // GL keep each exchange inside its group.
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
+// Diagnostic per-phase cycle counters (built only with -DDFLOP_TIMING, libdflop_timing.so):
+// 0 LPT, 1 refine j*/j', 2 refine member lists, 3 refine pairs, 4 refine reduce+apply,
+// 5 1F1B score, 6 loop/bookkeeping.
+struct PhaseTimer {
+#ifdef DFLOP_TIMING
+    unsigned long long* acc;
+    unsigned long long t0;
+    unsigned long long loc[8];
+    DFLOP_DEV void start(unsigned long long* a) {
+        acc = a;
+        t0 = clock64();
+        for (int k = 0; k < 8; ++k) loc[k] = 0;
+    }
+    DFLOP_DEV void mark(int k) {
+        const unsigned long long t1 = clock64();
+        loc[k] += t1 - t0;
+        t0 = t1;
+    }
+    DFLOP_DEV void flush(bool leader) {
+        if (leader && acc)
+            for (int k = 0; k < 8; ++k) atomicAdd(acc + k, loc[k]);
+    }
+#else
+    DFLOP_DEV void start(unsigned long long*) {}
+    DFLOP_DEV void mark(int) {}
+    DFLOP_DEV void flush(bool) {}
+#endif
+};
+
 template <typename A, int GL>
 DFLOP_DEV void argmin_reduce(A& v, uint32_t& j, unsigned mask) {
 #pragma unroll
@@ -339,7 +368,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
 // group of a warp issues the same shuffle sequence.
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
-                      uint8_t* apos, uint8_t* scr, uint16_t* spill, uint32_t gl, bool apply) {
+                      uint8_t* apos, uint8_t* scr, uint16_t* spill, uint32_t gl, bool apply, PhaseTimer& ph) {
     const uint32_t m = p.m, cap = p.cap;
     const bool wide = p.wide != 0;
     const uint32_t nblk = p.apos_bytes / 16;
@@ -368,6 +397,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         const Pair2<A> Bsp = EL[js], Bpp = EL[jp];
         const Pair2<A> Bs{unpack<A, PK>(Bsp.a, sh), unpack<A, PK>(Bsp.b, sh)};
         const Pair2<A> Bp{unpack<A, PK>(Bpp.a, sh), unpack<A, PK>(Bpp.b, sh)};
+        ph.mark(1);
         if (gl == 0) {
             cnt[0] = 0;
             cnt[1] = 0;
@@ -395,32 +425,55 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         __syncwarp(FULL);
         const uint32_t nA = cnt[0], nB = cnt[1];
         __syncwarp(FULL);
+        ph.mark(2);
         A bsc = amax<A>();
         uint32_t bi = 0xFFFFFFFFu, brk = 0xFFFFFFFFu;
         u64 bkey = ~0ull;  // 32-bit scores: (score << 32 | item << 16 | rank), a branch-free min
         const uint32_t nBs = min(nB, cap);
         // all (i, i') with i in j*, i' in {NONE} u j'; lexicographic min of (score, i, rank(i'))
-        for (uint32_t u = gl; u < nA; u += GL) {
+        // two j* members per lane and step: every j' member loaded once serves two pairs
+        auto ival = [&](uint32_t u, uint32_t& ii, A& se, A& sl, A& pe, A& pl) {
             const uint32_t pi = u < cap ? (uint32_t)ls[u] : (uint32_t)__ldcg(gss + (u - cap));
             const Pair2<A> a = T.el(pi);
-            const uint32_t ii = T.idx(pi);
-            const A se = Bs.a - a.a, sl = Bs.b - a.b;  // j* without i
-            const A pe = Bp.a + a.a, pl = Bp.b + a.b;  // j' with i
-            const A s0 = maxa(maxa(se, sl), maxa(pe, pl));
+            ii = T.idx(pi);
+            se = Bs.a - a.a;  // j* without i
+            sl = Bs.b - a.b;
+            pe = Bp.a + a.a;  // j' with i
+            pl = Bp.b + a.b;
+        };
+        for (uint32_t u = gl; u < nA; u += 2 * GL) {
+            uint32_t i0, i1;
+            A se0, sl0, pe0, pl0, se1, sl1, pe1, pl1;
+            ival(u, i0, se0, sl0, pe0, pl0);
+            if (u + GL < nA) {
+                ival(u + GL, i1, se1, sl1, pe1, pl1);
+            } else {  // duplicate of the first: same keys, no effect on the minimum
+                i1 = i0;
+                se1 = se0;
+                sl1 = sl0;
+                pe1 = pe0;
+                pl1 = pl0;
+            }
+            const A n0 = maxa(maxa(se0, sl0), maxa(pe0, pl0)), n1 = maxa(maxa(se1, sl1), maxa(pe1, pl1));
+            const u64 h0 = (u64)i0 << 16, h1 = (u64)i1 << 16;
+            if (sizeof(A) == 4) {
+                bkey = min(bkey, min(((u64)n0 << 32) | h0, ((u64)n1 << 32) | h1));
+            } else {
+                lex_update(bsc, bi, brk, n0, i0, 0u);
+                lex_update(bsc, bi, brk, n1, i1, 0u);
+            }
             auto pair = [&](uint32_t pj) {
                 const Pair2<A> b = T.el(pj);
                 const uint32_t rk = T.idx(pj) + 1u;
-                const A s1 = maxa<A>(se + b.a, sl + b.b);
-                const A s2 = maxa<A>(pe - b.a, pl - b.b);
-                if (sizeof(A) == 4)
-                    bkey = min(bkey, ((u64)maxa(s1, s2) << 32) | ((u64)ii << 16) | rk);
-                else
-                    lex_update(bsc, bi, brk, maxa(s1, s2), ii, rk);
+                const A s0 = maxa(maxa<A>(se0 + b.a, sl0 + b.b), maxa<A>(pe0 - b.a, pl0 - b.b));
+                const A s1 = maxa(maxa<A>(se1 + b.a, sl1 + b.b), maxa<A>(pe1 - b.a, pl1 - b.b));
+                if (sizeof(A) == 4) {
+                    bkey = min(bkey, min(((u64)s0 << 32) | h0 | rk, ((u64)s1 << 32) | h1 | rk));
+                } else {
+                    lex_update(bsc, bi, brk, s0, i0, rk);
+                    lex_update(bsc, bi, brk, s1, i1, rk);
+                }
             };
-            if (sizeof(A) == 4)
-                bkey = min(bkey, ((u64)s0 << 32) | ((u64)ii << 16));
-            else
-                lex_update(bsc, bi, brk, s0, ii, 0u);
             uint32_t v = 0;
             for (; v + 4 <= nBs; v += 4) {
                 const uint32_t q0 = lp[v], q1 = lp[v + 1], q2 = lp[v + 2], q3 = lp[v + 3];
@@ -430,8 +483,17 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 pair(q3);
             }
             for (; v < nBs; ++v) pair(lp[v]);
-            for (v = cap; v < nB; ++v) pair(__ldcg(gsp + (v - cap)));
+            for (v = cap; v + 4 <= nB; v += 4) {
+                const uint32_t q0 = __ldcg(gsp + (v - cap)), q1 = __ldcg(gsp + (v + 1 - cap));
+                const uint32_t q2 = __ldcg(gsp + (v + 2 - cap)), q3 = __ldcg(gsp + (v + 3 - cap));
+                pair(q0);
+                pair(q1);
+                pair(q2);
+                pair(q3);
+            }
+            for (v = max(v, cap); v < nB; ++v) pair(__ldcg(gsp + (v - cap)));
         }
+        ph.mark(3);
         if (sizeof(A) == 4) {
 #pragma unroll
             for (int off = GL / 2; off > 0; off >>= 1) bkey = min(bkey, __shfl_xor_sync(FULL, bkey, off));
@@ -465,6 +527,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             FL[jp] = fp;
         }
         __syncwarp(FULL);
+        ph.mark(4);
     }
 }
 
@@ -524,7 +587,7 @@ DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, c
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
                              Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* spill, uint32_t gl, u64& Tc,
-                             u64& cmax) {
+                             u64& cmax, PhaseTimer& ph) {
     const uint32_t m = p.m;
     for (uint32_t j = gl; j < m; j += GL) {
         EL[j] = PK ? Pair2<A>{(A)j, (A)j} : Pair2<A>{0, 0};
@@ -550,7 +613,8 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         __syncwarp(FULL);
     } else {
         lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, gl);
-        if (m >= 2) refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, spill, gl, c >= 2);
+        ph.mark(0);
+        if (m >= 2) refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, spill, gl, c >= 2, ph);
     }
     A cm = 0;
     for (uint32_t j = gl; j < m; j += GL) {
@@ -558,11 +622,13 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         cm = maxa(cm, unpack<A, PK>(maxa(el.a, el.b), sh));
     }
     cmax = (u64)max_reduce<A, GL>(cm, FULL);
+    ph.mark(6);
     Tc = score_1f1b<A, PK, GL>(p, sh, EL, FL, reinterpret_cast<u64*>(scr), gl);
+    ph.mark(5);
 }
 
 template <typename A, bool PK, int GL, bool SM>
-__global__ void __launch_bounds__(1024) k_candidates(CandParams p) {
+__global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     if (p.hdr->variant != p.want_variant) return;  // another variant runs
     const uint32_t sh = PK ? p.hdr->shift : 0u;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -600,12 +666,14 @@ __global__ void __launch_bounds__(1024) k_candidates(CandParams p) {
     __syncwarp(FULL);
     uint32_t cur = 0, best_buf = 0;
     u64 best_key = ~0ull, best_T = 0, best_cmax = 0;
+    PhaseTimer ph;
+    ph.start(p.phase);
     for (uint32_t c0 = p.c_begin + blockIdx.x * cpb; c0 < p.c_end; c0 += gridDim.x * cpb) {
         const bool valid = c0 + grp < p.c_end;
         const uint32_t c = valid ? c0 + grp : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
         u64 Tc, cmax;
-        run_candidate<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, spill, gl, Tc, cmax);
+        run_candidate<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, spill, gl, Tc, cmax, ph);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
         u64 key;
         if (Tc >= (1ull << 40)) {
@@ -627,6 +695,8 @@ __global__ void __launch_bounds__(1024) k_candidates(CandParams p) {
             cur ^= 1u;
         }
     }
+    ph.mark(6);
+    ph.flush(gl == 0);
     if (gl == 0) {
         p.slot_key[slot] = best_key;
         p.slot_T[slot] = best_T;

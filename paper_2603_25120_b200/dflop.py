@@ -12,7 +12,7 @@ import os
 from typing import Dict, Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdflop.so")
+LIB_PATH = os.environ.get("DFLOP_LIB") or os.path.join(HERE, "libdflop.so")
 
 MAX_X, MAX_TP = 32, 4
 MODE_HEURISTIC, MODE_EXHAUSTIVE = 0, 1

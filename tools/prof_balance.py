@@ -36,3 +36,10 @@ for rep in range(a.reps):
     best = D.cand_result(r["best"])
     print(f"rep {rep}: K={a.K} R={R} {ms:.2f} ms  {a.K / ms * 1e3:.0f} cand/s  best c={best['cand']} T={best['makespan']}",
           flush=True)
+    if "timing" in D.LIB_PATH:  # diagnostic build: per-phase cycles of the candidate kernel
+        import ctypes
+        out = (ctypes.c_ulonglong * 8)()
+        D.lib().dflop_debug_phase_cycles(out, 1)
+        tot = sum(out) or 1
+        names = ["lpt", "ref_jstar", "ref_lists", "ref_pairs", "ref_apply", "score", "other", "-"]
+        print("   phases: " + "  ".join(f"{nm}={v / tot * 100:.1f}%" for nm, v in zip(names, out) if v), flush=True)
