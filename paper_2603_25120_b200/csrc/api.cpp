@@ -459,7 +459,7 @@ static size_t balance_bound(uint32_t n, uint32_t m_max, uint32_t K, int device) 
     const size_t apos_max = std::max<size_t>(16, ((size_t)2 * n + 15) & ~(size_t)15);
     return 256 * 2 + al256((size_t)n * 8) + 2 * al256((size_t)n * 4) + al256((size_t)n * 16) +
            al256((size_t)n * 32) + 3 * al256(slots * 8) + al256(slots * 4) + al256(slots * 2 * apos_max) +
-           al256(slots * 4 * (size_t)std::max(1u, n)) + al256((size_t)m_max * 4) * 2 + 4096;
+           al256(slots * 4 * ((size_t)n + 512)) + al256((size_t)m_max * 4) * 2 + 4096;
 }
 
 static SearchLayout search_layout(uint32_t n, uint32_t P, uint64_t n_pairs, size_t bal_bytes, int device) {

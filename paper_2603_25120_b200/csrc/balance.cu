@@ -366,7 +366,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     cfg.o_slot_cmax = o;  o += align256((size_t)cfg.n_slots * 8);
     cfg.o_slot_buf = o;   o += align256((size_t)cfg.n_slots * 4);
     cfg.o_slot_apos = o;  o += align256((size_t)cfg.n_slots * 2 * cfg.apos_bytes);
-    cfg.o_slot_spill = o; o += align256((size_t)cfg.n_slots * 4 * std::max(1u, n));
+    cfg.o_slot_spill = o; o += align256((size_t)cfg.n_slots * 4 * ((size_t)n + 512));
     cfg.o_grp = o;        o += groups_ws_bytes(n, m);
     cfg.total = o;
     cfg.ok = true;

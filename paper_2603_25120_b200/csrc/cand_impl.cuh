@@ -317,16 +317,31 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                 // keys (W << s) | j: one fused add-max and one min per probe
                 const uint32_t es = ((uint32_t)it.e << sh) & (uint32_t)use, ls = ((uint32_t)it.l << sh) & (uint32_t)use;
                 uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
-                uint32_t j = gl;
+                if (m <= 8 * GL) {  // every preset: at most 8 buckets per lane, fully unrolled
+#pragma unroll
+                    for (uint32_t k = 0; k < 8; k += 2) {
+                        const uint32_t j0 = gl + GL * k, j1 = j0 + GL;
+                        if (j0 < m) {
+                            const Pair2<A> x = EL[j0];
+                            b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                        }
+                        if (j1 < m) {
+                            const Pair2<A> y = EL[j1];
+                            b1 = min(b1, max((uint32_t)y.a + es, (uint32_t)y.b + ls));
+                        }
+                    }
+                } else {
+                    uint32_t j = gl;
 #pragma unroll 4
-                for (; j + GL < m; j += 2 * GL) {
-                    const Pair2<A> x = EL[j], y = EL[j + GL];
-                    b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
-                    b1 = min(b1, max((uint32_t)y.a + es, (uint32_t)y.b + ls));
-                }
-                if (j < m) {
-                    const Pair2<A> x = EL[j];
-                    b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                    for (; j + GL < m; j += 2 * GL) {
+                        const Pair2<A> x = EL[j], y = EL[j + GL];
+                        b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                        b1 = min(b1, max((uint32_t)y.a + es, (uint32_t)y.b + ls));
+                    }
+                    if (j < m) {
+                        const Pair2<A> x = EL[j];
+                        b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                    }
                 }
                 uint32_t best = min(b0, b1);
 #pragma unroll
@@ -347,7 +362,9 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                 }
                 argmin_reduce<A, GL>(bv, bj, FULL);
             }
-            if (gl == 0) {
+            // during LPT bucket j is read and written only by its owner lane j % GL, so the
+            // update needs no warp barrier (the shuffles already order the lanes)
+            if ((bj & (GL - 1)) == gl) {
                 Pair2<A> el = EL[bj], fl = FL[bj];
                 el.a += PK ? (A)((uint32_t)it.e << sh) : it.e;
                 el.b += PK ? (A)((uint32_t)it.l << sh) : it.l;
@@ -357,10 +374,10 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                 FL[bj] = fl;
                 set_apos(apos, pos, bj, wide);
             }
-            __syncwarp(FULL);
         }
       }
     }
+    __syncwarp(FULL);
 }
 
 // ---------------------------------------------------------------- swap refinement (O6)
@@ -376,7 +393,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
     uint16_t* ls = reinterpret_cast<uint16_t*>(scr + 16);
     uint16_t* lp = ls + cap;
     uint16_t* gss = spill;           // global spill of ls
-    uint16_t* gsp = spill + p.n;     // global spill of lp
+    uint16_t* gsp = spill + p.n + 512;  // global spill of lp (a lane column holds <= n/GL + 16 rows)
     for (uint32_t r = 0; r < p.R; ++r) {
         // bottleneck bucket j* = lowest j with maximal W_j = max(E_j, L_j)
         A Wb = 0;
@@ -403,24 +420,35 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             cnt[1] = 0;
         }
         __syncwarp(FULL);
-        // member lists of j* (ls) and j' (lp): 16-byte L2 scans of the assignment, 4 in flight;
+        // member lists of j* (ls) and j' (lp): 16-byte L2 scans of the assignment, double
+        // buffered (the next SB blocks are in flight while the current ones are processed);
         // entries past the shared-memory capacity spill to the slot's global area
-        for (uint32_t b0 = gl; b0 < nblk; b0 += 4 * GL) {
-            uint4 v[4];
+        {
+            constexpr int SB = 4;
+            uint4 cur[SB], nxt[SB];
+            auto load = [&](uint4* v, uint32_t b0) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t b = b0 + u * GL;
-                v[u] = b < nblk ? __ldcg(reinterpret_cast<const uint4*>(apos) + b) : make_uint4(~0u, ~0u, ~0u, ~0u);
+                for (int u = 0; u < SB; ++u) {
+                    const uint32_t b = b0 + u * GL;
+                    v[u] = b < nblk ? __ldcg(reinterpret_cast<const uint4*>(apos) + b)
+                                    : make_uint4(~0u, ~0u, ~0u, ~0u);
+                }
+            };
+            load(cur, gl);
+            for (uint32_t b0 = gl; b0 < nblk; b0 += SB * GL) {
+                if (b0 + SB * GL < nblk) load(nxt, b0 + SB * GL);
+#pragma unroll
+                for (int u = 0; u < SB; ++u)
+                    scan_words(cur[u], b0 + u * GL, wide, js, jp, [&](uint32_t pos, int which) {
+                        const uint32_t at = atomicAdd(&cnt[which], 1u);
+                        if (at < cap)
+                            (which ? lp : ls)[at] = (uint16_t)pos;
+                        else
+                            (which ? gsp : gss)[at - cap] = (uint16_t)pos;
+                    });
+#pragma unroll
+                for (int u = 0; u < SB; ++u) cur[u] = nxt[u];
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                scan_words(v[u], b0 + u * GL, wide, js, jp, [&](uint32_t pos, int which) {
-                    const uint32_t at = atomicAdd(&cnt[which], 1u);
-                    if (at < cap)
-                        (which ? lp : ls)[at] = (uint16_t)pos;
-                    else
-                        (which ? gsp : gss)[at - cap] = (uint16_t)pos;
-                });
         }
         __syncwarp(FULL);
         const uint32_t nA = cnt[0], nB = cnt[1];
@@ -656,7 +684,7 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     uint8_t* scr = base + p.off_scr;
     const uint32_t slot = blockIdx.x * cpb + grp;
     uint8_t* bufs = p.slot_apos + (size_t)slot * 2 * p.apos_bytes;
-    uint16_t* spill = p.slot_spill + (size_t)slot * 2 * p.n;
+    uint16_t* spill = p.slot_spill + (size_t)slot * 2 * (p.n + 512);
     // padding past n never matches a bucket (0xFF / 0xFFFF)
     const uint32_t used = p.n * (p.wide ? 2u : 1u);
     for (uint32_t b = used + gl; b < p.apos_bytes; b += GL) {
