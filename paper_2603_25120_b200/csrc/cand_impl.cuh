@@ -296,7 +296,7 @@ template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
                         Pair2<A>* FL, uint8_t* apos, uint32_t gl) {
     const uint32_t n = p.n, m = p.m, G = p.G;
-    const bool wide = p.wide != 0;
+    const bool wide = PK ? false : p.wide != 0;  // the packed variant requires m <= 255
     const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
     const uint32_t jmask = (1u << sh) - 1u;
     const uint32_t nc = (G - 1 + 3) / 4;  // Philox calls per group
@@ -317,7 +317,14 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                 // keys (W << s) | j: one fused add-max and one min per probe
                 const uint32_t es = ((uint32_t)it.e << sh) & (uint32_t)use, ls = ((uint32_t)it.l << sh) & (uint32_t)use;
                 uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
-                if (m <= 8 * GL) {  // every preset: at most 8 buckets per lane, fully unrolled
+                if (m == 8 * GL) {  // every preset: exactly 8 buckets per lane, no bounds tests
+#pragma unroll
+                    for (uint32_t k = 0; k < 8; k += 2) {
+                        const Pair2<A> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
+                        b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                        b1 = min(b1, max((uint32_t)y.a + es, (uint32_t)y.b + ls));
+                    }
+                } else if (m < 8 * GL) {  // at most 8 buckets per lane, fully unrolled
 #pragma unroll
                     for (uint32_t k = 0; k < 8; k += 2) {
                         const uint32_t j0 = gl + GL * k, j1 = j0 + GL;
@@ -387,7 +394,7 @@ template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
                       uint8_t* apos, uint8_t* scr, uint16_t* spill, uint32_t gl, bool apply, PhaseTimer& ph) {
     const uint32_t m = p.m, cap = p.cap;
-    const bool wide = p.wide != 0;
+    const bool wide = PK ? false : p.wide != 0;  // the packed variant requires m <= 255
     const uint32_t nblk = p.apos_bytes / 16;
     uint32_t* cnt = reinterpret_cast<uint32_t*>(scr);
     uint16_t* ls = reinterpret_cast<uint16_t*>(scr + 16);
