@@ -37,16 +37,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=(), timing: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra=(), timing: bool = False, variant: str = "") -> str:
     """timing=True builds libdflop_timing.so with -DDFLOP_TIMING (per-phase clock64 counters
-    in the candidate kernel, read with dflop_debug_phase_cycles); a diagnostic build only."""
-    lib = os.path.join(HERE, "libdflop_timing.so") if timing else LIB
+    in the candidate kernel, read with dflop_debug_phase_cycles); a diagnostic build only.
+    variant="x" with extra=("-DFOO",) builds libdflop_x.so (A/B experiments, loaded through
+    the DFLOP_LIB environment variable)."""
     if timing:
+        variant = variant or "timing"
         extra = tuple(extra) + ("-DDFLOP_TIMING",)
-    if not force and not timing and not _stale():
+    lib = os.path.join(HERE, f"libdflop_{variant}.so") if variant else LIB
+    if not force and not variant and not _stale():
         return LIB
     inc, libdir = _nccl_dirs()
-    objdir = os.path.join(HERE, "build_timing" if timing else "build")
+    objdir = os.path.join(HERE, f"build_{variant}" if variant else "build")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + inc, "-I" + os.path.join(ROOT, "include"),
               *ARCH, *extra]

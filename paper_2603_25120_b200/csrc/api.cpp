@@ -26,6 +26,7 @@ struct dflop_comm {
 namespace dflop {
 
 static thread_local std::string g_err;
+static void release_streams();
 
 void set_error(const char* fmt, ...) {
     char buf[512];
@@ -189,6 +190,7 @@ const char* dflop_last_error(void) { return g_err.c_str(); }
 
 dflop_status dflop_release_caches(void) {
     release_slot_programs();
+    release_streams();
     return DFLOP_OK;
 }
 
@@ -446,8 +448,38 @@ static int owner_of(uint32_t K, uint32_t c, int G) {
 // workspace regions of the search
 struct SearchLayout {
     size_t o_costs, o_results, o_assigns, o_bcast, o_key, o_stage_a, o_top, o_feas, o_status, o_bal, total;
-    size_t bal_bytes;
+    size_t bal_bytes, bal_stride;
+    uint32_t n_bal;  // balance workspaces: one per Stage-B stream
 };
+
+// Stage B balances the top-P plans on up to kStageBStreams streams: one plan's candidate
+// kernel runs ~1.7 waves of the GPU, so the tail of one plan overlaps the next plan's start
+// (DESIGN.md section 9).  DFLOP_STAGEB_STREAMS=1..8 overrides.
+constexpr uint32_t kStageBStreams = 4;
+static uint32_t stage_b_streams() {
+    const char* e = getenv("DFLOP_STAGEB_STREAMS");
+    const int v = e ? atoi(e) : (int)kStageBStreams;
+    return (uint32_t)std::min(8, std::max(1, v));
+}
+static std::mutex g_stream_mu;
+static std::map<int, std::vector<cudaStream_t>> g_streams;
+// k-th auxiliary stream of `dev` (created once, non-blocking, destroyed by dflop_release_caches)
+static cudaStream_t aux_stream(int dev, uint32_t k) {
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    auto& v = g_streams[dev];
+    while (v.size() <= k) {
+        cudaStream_t st = nullptr;
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        v.push_back(st);
+    }
+    return v[k];
+}
+static void release_streams() {
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    for (auto& kv : g_streams)
+        for (cudaStream_t st : kv.second) cudaStreamDestroy(st);
+    g_streams.clear();
+}
 
 // Upper bound of one balance workspace when the plan is not known yet (Algorithm 1 mode):
 // at most one resident candidate group per candidate of the shard plus one warp of groups
@@ -459,10 +491,11 @@ static size_t balance_bound(uint32_t n, uint32_t m_max, uint32_t K, int device) 
     const size_t apos_max = std::max<size_t>(16, ((size_t)2 * n + 15) & ~(size_t)15);
     return 256 * 2 + al256((size_t)n * 8) + 2 * al256((size_t)n * 4) + al256((size_t)n * 16) +
            al256((size_t)n * 32) + 3 * al256(slots * 8) + al256(slots * 4) + al256(slots * 2 * apos_max) +
-           al256(slots * 4 * ((size_t)n + 512)) + al256((size_t)m_max * 4) * 2 + 4096;
+           al256(slots * 2 * (2 * (size_t)n + 5 * (size_t)m_max + 16)) + al256((size_t)m_max * 4) * 2 + 4096;
 }
 
-static SearchLayout search_layout(uint32_t n, uint32_t P, uint64_t n_pairs, size_t bal_bytes, int device) {
+static SearchLayout search_layout(uint32_t n, uint32_t P, uint64_t n_pairs, size_t bal_bytes, uint32_t n_bal,
+                                  int device) {
     SearchLayout L;
     size_t o = 0;
     L.o_costs = o;   o += al256((size_t)P * 4 * n * 4);
@@ -475,7 +508,9 @@ static SearchLayout search_layout(uint32_t n, uint32_t P, uint64_t n_pairs, size
     L.o_feas = o;    o += 256;
     L.o_status = o;  o += 256;
     L.bal_bytes = bal_bytes;
-    L.o_bal = o;     o += al256(L.bal_bytes);
+    L.bal_stride = al256(bal_bytes);
+    L.n_bal = std::max(1u, n_bal);
+    L.o_bal = o;     o += L.bal_stride * L.n_bal;
     L.total = o;
     return L;
 }
@@ -544,7 +579,8 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
             return st;
         bal_bytes = bp0.cfg.total;
     }
-    const SearchLayout L = search_layout(n, P, tab ? tab->n_pairs : 0, bal_bytes, dev);
+    const SearchLayout L =
+        search_layout(n, P, tab ? tab->n_pairs : 0, bal_bytes, alg1 ? std::min(P, stage_b_streams()) : 1u, dev);
     if (!ws) {
         *ws_bytes = L.total;
         return DFLOP_OK;
@@ -618,11 +654,36 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
     if (ce != cudaSuccess) return cuda_status(ce, "predict launch");
     uint32_t cb, cend;
     shard(sp->K, g, G, &cb, &cend);
+    // fork: plan p runs on stream p % ns with balance workspace p % ns; joined below
+    const uint32_t ns = std::min<uint32_t>(L.n_bal, np);
+    std::vector<cudaStream_t> ss(ns, s);
+    struct Events {
+        std::vector<cudaEvent_t> ev;
+        ~Events() {
+            for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        }
+        cudaEvent_t make() {
+            cudaEvent_t e = nullptr;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+            ev.push_back(e);
+            return e;
+        }
+    } evs;
+    if (ns > 1) {
+        cudaEvent_t fork = evs.make();
+        if (!fork || cudaEventRecord(fork, s) != cudaSuccess) return cuda_status(cudaGetLastError(), "fork event");
+        for (uint32_t k = 1; k < ns; ++k) {
+            ss[k] = aux_stream(dev, k - 1);
+            if (!ss[k]) return cuda_status(cudaGetLastError(), "stage B stream");
+            if ((ce = cudaStreamWaitEvent(ss[k], fork, 0)) != cudaSuccess) return cuda_status(ce, "fork wait");
+        }
+    }
     for (uint32_t p = 0; p < np; ++p) {
         BalancePlan bpn;
+        cudaStream_t sp_s = ss[p % ns];
         if (cb >= cend) {
             // empty shard on this rank: mark the plan's result as "no candidate"
-            ce = cudaMemsetAsync(&results[p], 0xFF, sizeof(dflop_cand_result), s);
+            ce = cudaMemsetAsync(&results[p], 0xFF, sizeof(dflop_cand_result), sp_s);
             if (ce != cudaSuccess) return cuda_status(ce, "memset");
             continue;
         }
@@ -641,10 +702,15 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
         a.seed0 = sp->seed[0];
         a.seed1 = sp->seed[1];
         a.id_base = p * sp->K;
-        a.ws = bal_ws;
+        a.ws = reinterpret_cast<char*>(bal_ws) + (size_t)(p % ns) * L.bal_stride;
         a.best = &results[p];
         a.assign = assigns + (size_t)p * n;
-        if ((st = balance_launch(a, bpn.cfg, bpn.prog, s)) != DFLOP_OK) return st;
+        if ((st = balance_launch(a, bpn.cfg, bpn.prog, sp_s)) != DFLOP_OK) return st;
+    }
+    for (uint32_t k = 1; k < ns; ++k) {  // join
+        cudaEvent_t j = evs.make();
+        if (!j || cudaEventRecord(j, ss[k]) != cudaSuccess) return cuda_status(cudaGetLastError(), "join event");
+        if ((ce = cudaStreamWaitEvent(s, j, 0)) != cudaSuccess) return cuda_status(ce, "join wait");
     }
     // ---- local argmin over plans, then the NCCL min all-reduce of the packed key
     std::vector<dflop_cand_result> hres(np);

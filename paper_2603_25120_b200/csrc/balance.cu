@@ -299,13 +299,23 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) gl = forced;
     cfg.gl = gl;
     const uint32_t per_bucket = (n + m - 1) / std::max(1u, m);
-    uint32_t cap = std::min(256u, std::max(32u, next_pow2(3 * std::max(1u, per_bucket))));
+    uint32_t cap = std::min(128u, std::max(32u, next_pow2(2 * std::max(1u, per_bucket))));
     const int forced_cap = env_int("DFLOP_CAP", 0);
     if (forced_cap >= 1 && forced_cap <= 4096) cap = (uint32_t)forced_cap;
     cfg.cap = cap;
     const bool wide = m > 255;
     cfg.apos_bytes = round16(std::max(16u, n * (wide ? 2u : 1u)));
-    const uint32_t scr = round16(std::max(16u + 4u * cfg.cap, (S + 2 * S * sh.D) * 8u));
+    // CSR member lists of the refinement: every bucket gets its LPT
+    // count plus sigma free entries (a move adds one member to j'); a list that would
+    // overflow triggers a rebuild from the assignment
+    cfg.sigma = std::max(1u, std::min(std::max(1u, sh.R), per_bucket));
+    // counters cnt[m] and offsets off[m + 1] (u32) in shared memory up to m = 256, else in
+    // front of the slot's global lists
+    cfg.cnt_smem = m <= 256;
+    const size_t hdr_u16 = cfg.cnt_smem ? 0 : 2 * (2 * (size_t)m + 1);
+    cfg.csr_len = (uint32_t)((hdr_u16 + (size_t)n + (size_t)m * cfg.sigma + 7) & ~(size_t)7);
+    // scratch: [cnt, off,] ls[cap], lp[cap] (u16) -- or the 1F1B rings
+    const uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cfg.cap, (S + 2 * S * sh.D) * 8u));
     const size_t smem_max = prop.smem_optin;
     const uint32_t nsm = (uint32_t)prop.sms;
     const uint32_t per_warp = 32u / (uint32_t)gl;  // candidate groups per warp
@@ -367,7 +377,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     cfg.o_slot_cmax = o;  o += align256((size_t)cfg.n_slots * 8);
     cfg.o_slot_buf = o;   o += align256((size_t)cfg.n_slots * 4);
     cfg.o_slot_apos = o;  o += align256((size_t)cfg.n_slots * 2 * cfg.apos_bytes);
-    cfg.o_slot_spill = o; o += align256((size_t)cfg.n_slots * 4 * ((size_t)n + 512));
+    cfg.o_slot_csr = o;   o += align256((size_t)cfg.n_slots * 2 * cfg.csr_len);
     cfg.o_grp = o;        o += groups_ws_bytes(n, m);
     cfg.total = o;
     cfg.ok = true;
@@ -388,7 +398,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     u64* slot_cmax = reinterpret_cast<u64*>(ws + cfg.o_slot_cmax);
     uint32_t* slot_buf = reinterpret_cast<uint32_t*>(ws + cfg.o_slot_buf);
     uint8_t* slot_apos = reinterpret_cast<uint8_t*>(ws + cfg.o_slot_apos);
-    uint16_t* slot_spill = reinterpret_cast<uint16_t*>(ws + cfg.o_slot_spill);
+    uint16_t* slot_csr = reinterpret_cast<uint16_t*>(ws + cfg.o_slot_csr);
     const uint32_t n = a.sh.n;
     const uint32_t allow_pack = a.sh.mode == DFLOP_MODE_EXHAUSTIVE ? 0u : 1u;
 
@@ -410,7 +420,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     p.n_levels = prog.n_levels;
     p.hdr = hdr;
     p.slot_apos = slot_apos;
-    p.slot_spill = slot_spill;
+    p.slot_csr = slot_csr;
     p.slot_key = slot_key;
     p.slot_T = slot_T;
     p.slot_cmax = slot_cmax;
@@ -435,6 +445,9 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     p.exhaustive = a.sh.mode == DFLOP_MODE_EXHAUSTIVE;
     p.wide = a.sh.m > 255;
     p.cap = cfg.cap;
+    p.sigma = cfg.sigma;
+    p.cnt_smem = cfg.cnt_smem ? 1u : 0u;
+    p.csr_len = cfg.csr_len;
     p.apos_bytes = cfg.apos_bytes;
     p.phase = phase_counters();
     const int mark = prof_begin(s);

@@ -18,7 +18,8 @@ constexpr int kCandMaxThreads = 640;
 //   [0, tbl_bytes)              CTA item table: ItemRec<A>[n] then u16 pos->item[n]
 //   tbl_bytes + g*cand_bytes    candidate group g: EL[m] {E, L}, FL[m] {EF, LF}, scratch
 // Global: per resident group ("slot") two assignment buffers of apos_bytes (u8 per base-order
-// position when m <= 255, else u16), the best one named by slot_buf[slot].
+// position when m <= 255, else u16), the best one named by slot_buf[slot], and the CSR
+// member lists of the refinement (csr_len u16 positions).
 struct CandParams {
     const void* items;           // ItemRec<A>[n], base-order positions (global)
     const uint32_t* pos_item;    // [n] position -> item index (global)
@@ -27,7 +28,7 @@ struct CandParams {
     const uint32_t* levels;      // n_levels + 1 offsets into ops
     BalanceHeader* hdr;
     uint8_t* slot_apos;          // [n_slots][2][apos_bytes]
-    uint16_t* slot_spill;        // [n_slots][2][n] refinement-list overflow
+    uint16_t* slot_csr;          // [n_slots][csr_len] refinement member lists (positions, CSR)
     u64* slot_key;
     u64* slot_T;
     u64* slot_cmax;
@@ -36,7 +37,8 @@ struct CandParams {
     u64* cand_cmax;
     uint32_t n, m, S, e_pp, l_dp, n_mb, R, G, D, n_ops, n_levels;
     uint32_t c_begin, c_end, id_base, seed0, seed1;
-    uint32_t exhaustive, wide, cap, apos_bytes, want_variant;
+    uint32_t exhaustive, wide, cap, sigma, csr_len, apos_bytes, want_variant;
+    uint32_t cnt_smem;           // refinement list counters in shared memory (else global)
     uint32_t tbl_bytes, cand_bytes, off_fl, off_scr;
     unsigned long long* phase;   // diagnostic phase counters (timing builds), else null
 };

@@ -244,49 +244,81 @@ DFLOP_DEV void set_apos(uint8_t* apos, uint32_t pos, uint32_t j, bool wide) {
         apos[pos] = (uint8_t)j;
 }
 
-// Processes one 16-byte block of the assignment (16 positions u8 / 8 positions u16) and calls
-// f(pos, which) for every position assigned to ja (which = 0) or jb (which = 1).  A word
-// is inspected byte by byte only when the zero-byte test of (word ^ target) fires, which is
-// exact as a predicate: (x - 0x01..01) & ~x & 0x80..80 != 0 iff some byte of x is zero.
+// Calls f(pos, j) for the entries of one 16-byte block of the assignment (16 u8 or 8 u16
+// positions); padding past n holds 0xFF / 0xFFFF, never a bucket (m <= 255 / m <= 65535).
 template <typename F>
-DFLOP_DEV void scan_words(const uint4 v, uint32_t blk, bool wide, uint32_t ja, uint32_t jb, F&& f) {
+DFLOP_DEV void each_entry(const uint4 v, uint32_t blk, bool wide, uint32_t m, F&& f) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     if (!wide) {
-        const uint32_t A4 = ja * 0x01010101u, B4 = jb * 0x01010101u;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t x = w[k] ^ A4, y = w[k] ^ B4;
-            const uint32_t h = ((x - 0x01010101u) & ~x) | ((y - 0x01010101u) & ~y);
-            if (h & 0x80808080u) {
+        for (int k = 0; k < 4; ++k)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const uint32_t val = (w[k] >> (8 * b)) & 0xFFu;
-                    if (val == ja) f(blk * 16 + 4 * k + b, 0);
-                    else if (val == jb) f(blk * 16 + 4 * k + b, 1);
-                }
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t j = (w[k] >> (8 * b)) & 0xFFu;
+                if (j < m) f(blk * 16 + 4 * k + b, j);
             }
-        }
     } else {
-        const uint32_t A2 = ja * 0x00010001u, B2 = jb * 0x00010001u;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t x = w[k] ^ A2, y = w[k] ^ B2;
-            const uint32_t h = ((x - 0x00010001u) & ~x) | ((y - 0x00010001u) & ~y);
-            if (h & 0x80008000u) {
+        for (int k = 0; k < 4; ++k)
 #pragma unroll
-                for (int b = 0; b < 2; ++b) {
-                    const uint32_t val = (w[k] >> (16 * b)) & 0xFFFFu;
-                    if (val == ja) f(blk * 8 + 2 * k + b, 0);
-                    else if (val == jb) f(blk * 8 + 2 * k + b, 1);
-                }
+            for (int b = 0; b < 2; ++b) {
+                const uint32_t j = (w[k] >> (16 * b)) & 0xFFFFu;
+                if (j < m) f(blk * 8 + 2 * k + b, j);
             }
-        }
     }
 }
 
-template <typename F>
-DFLOP_DEV void scan_block(const uint8_t* apos, uint32_t blk, bool wide, uint32_t ja, uint32_t jb, F&& f) {
-    scan_words(__ldcg(reinterpret_cast<const uint4*>(apos) + blk), blk, wide, ja, jb, f);
+// CSR member lists of all m buckets from the assignment: cnt[j] members of bucket j at
+// csr[off[j] ..], off[j+1] - off[j] = (LPT count) + sigma.  Two 16-byte L2 passes (count,
+// then scatter); the list order is irrelevant (the pair search is a keyed minimum).
+template <int GL>
+DFLOP_DEV void build_lists(const CandParams& p, const uint8_t* apos, bool wide, uint32_t* cnt, uint32_t* off,
+                           uint16_t* csr, uint32_t gl) {
+    const uint32_t m = p.m, nblk = p.apos_bytes / 16, sig = p.sigma;
+    const uint4* ap = reinterpret_cast<const uint4*>(apos);
+    for (uint32_t j = gl; j < m; j += GL) cnt[j] = 0;
+    __syncwarp(FULL);
+    for (uint32_t b = gl; b < nblk; b += GL)
+        each_entry(__ldcg(ap + b), b, wide, m, [&](uint32_t, uint32_t j) { atomicAdd(&cnt[j], 1u); });
+    __syncwarp(FULL);
+    // exclusive prefix of cnt[j] + sigma, GL buckets per step (coalesced when the counters
+    // live in global memory); counters reset for the scatter pass
+    uint32_t run = 0;
+    for (uint32_t j0 = 0; j0 < m; j0 += GL) {
+        const uint32_t j = j0 + gl;
+        const uint32_t v = j < m ? cnt[j] + sig : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int d = 1; d < GL; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, inc, d, GL);
+            if (gl >= (uint32_t)d) inc += y;
+        }
+        if (j < m) {
+            off[j] = run + inc - v;
+            cnt[j] = 0;
+        }
+        run += __shfl_sync(FULL, inc, GL - 1, GL);
+    }
+    if (gl == 0) off[m] = run;
+    __syncwarp(FULL);
+    for (uint32_t b = gl; b < nblk; b += GL)
+        each_entry(__ldcg(ap + b), b, wide, m, [&](uint32_t pos, uint32_t j) {
+            const uint32_t at = atomicAdd(&cnt[j], 1u);
+            csr[off[j] + at] = (uint16_t)pos;
+        });
+    __syncwarp(FULL);
+}
+
+// Q buckets per lane (m == Q*GL), fully unrolled: two running minima of the packed keys
+template <int Q, int GL>
+DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t es, uint32_t ls, uint32_t& b0,
+                           uint32_t& b1) {
+#pragma unroll
+    for (uint32_t k = 0; k < Q; k += 2) {
+        const Pair2<uint32_t> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
+        b0 = min(b0, max(x.a + es, x.b + ls));
+        b1 = min(b1, max(y.a + es, y.b + ls));
+    }
 }
 
 // ---------------------------------------------------------------- LPT pass (R12)
@@ -318,12 +350,11 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                 const uint32_t es = ((uint32_t)it.e << sh) & (uint32_t)use, ls = ((uint32_t)it.l << sh) & (uint32_t)use;
                 uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
                 if (m == 8 * GL) {  // every preset: exactly 8 buckets per lane, no bounds tests
-#pragma unroll
-                    for (uint32_t k = 0; k < 8; k += 2) {
-                        const Pair2<A> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
-                        b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
-                        b1 = min(b1, max((uint32_t)y.a + es, (uint32_t)y.b + ls));
-                    }
+                    probe_fixed<8, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, es, ls, b0, b1);
+                } else if (m == 16 * GL) {
+                    probe_fixed<16, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, es, ls, b0, b1);
+                } else if (m == 32 * GL) {
+                    probe_fixed<32, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, es, ls, b0, b1);
                 } else if (m < 8 * GL) {  // at most 8 buckets per lane, fully unrolled
 #pragma unroll
                     for (uint32_t k = 0; k < 8; k += 2) {
@@ -392,16 +423,30 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
 // group of a warp issues the same shuffle sequence.
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
-                      uint8_t* apos, uint8_t* scr, uint16_t* spill, uint32_t gl, bool apply, PhaseTimer& ph) {
+                      uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, bool apply, PhaseTimer& ph) {
     const uint32_t m = p.m, cap = p.cap;
     const bool wide = PK ? false : p.wide != 0;  // the packed variant requires m <= 255
-    const uint32_t nblk = p.apos_bytes / 16;
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(scr);
-    uint16_t* ls = reinterpret_cast<uint16_t*>(scr + 16);
+    // cnt[m] members per bucket, off[m + 1] list starts: in shared memory (m <= 256), else
+    // in front of the slot's global lists; then the shared-memory copies of the first cap
+    // members of j* (ls) and j' (lp)
+    uint32_t* cnt;
+    uint16_t* ls;
+    if (p.cnt_smem) {
+        cnt = reinterpret_cast<uint32_t*>(scr);
+        ls = reinterpret_cast<uint16_t*>(cnt + 2 * m + 1);
+    } else {
+        cnt = reinterpret_cast<uint32_t*>(csr);
+        csr += 2 * (2 * m + 1);
+        ls = reinterpret_cast<uint16_t*>(scr);
+    }
+    uint32_t* off = cnt + m;
     uint16_t* lp = ls + cap;
-    uint16_t* gss = spill;           // global spill of ls
-    uint16_t* gsp = spill + p.n + 512;  // global spill of lp (a lane column holds <= n/GL + 16 rows)
+    bool dirty = true;  // the lists must be (re)built from the assignment
     for (uint32_t r = 0; r < p.R; ++r) {
+        if (__any_sync(FULL, dirty)) {  // warp-uniform: a clean group rebuilds the same lists
+            build_lists<GL>(p, apos, wide, cnt, off, csr, gl);
+            dirty = false;
+        }
         // bottleneck bucket j* = lowest j with maximal W_j = max(E_j, L_j)
         A Wb = 0;
         uint32_t jb = 0xFFFFFFFFu;
@@ -422,43 +467,16 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         const Pair2<A> Bs{unpack<A, PK>(Bsp.a, sh), unpack<A, PK>(Bsp.b, sh)};
         const Pair2<A> Bp{unpack<A, PK>(Bpp.a, sh), unpack<A, PK>(Bpp.b, sh)};
         ph.mark(1);
-        if (gl == 0) {
-            cnt[0] = 0;
-            cnt[1] = 0;
-        }
-        __syncwarp(FULL);
-        // member lists of j* (ls) and j' (lp): 16-byte L2 scans of the assignment, double
-        // buffered (the next SB blocks are in flight while the current ones are processed);
-        // entries past the shared-memory capacity spill to the slot's global area
+        // member lists of j* (gss) and j' (gsp); their first cap entries are copied to
+        // shared memory (ls, lp), the rest is read from L2
+        const uint32_t nA = cnt[js], nB = cnt[jp];
+        uint16_t* gss = csr + off[js];
+        uint16_t* gsp = csr + off[jp];
         {
-            constexpr int SB = 4;
-            uint4 cur[SB], nxt[SB];
-            auto load = [&](uint4* v, uint32_t b0) {
-#pragma unroll
-                for (int u = 0; u < SB; ++u) {
-                    const uint32_t b = b0 + u * GL;
-                    v[u] = b < nblk ? __ldcg(reinterpret_cast<const uint4*>(apos) + b)
-                                    : make_uint4(~0u, ~0u, ~0u, ~0u);
-                }
-            };
-            load(cur, gl);
-            for (uint32_t b0 = gl; b0 < nblk; b0 += SB * GL) {
-                if (b0 + SB * GL < nblk) load(nxt, b0 + SB * GL);
-#pragma unroll
-                for (int u = 0; u < SB; ++u)
-                    scan_words(cur[u], b0 + u * GL, wide, js, jp, [&](uint32_t pos, int which) {
-                        const uint32_t at = atomicAdd(&cnt[which], 1u);
-                        if (at < cap)
-                            (which ? lp : ls)[at] = (uint16_t)pos;
-                        else
-                            (which ? gsp : gss)[at - cap] = (uint16_t)pos;
-                    });
-#pragma unroll
-                for (int u = 0; u < SB; ++u) cur[u] = nxt[u];
-            }
+            const uint32_t na = min(nA, cap), nb = min(nB, cap);
+            for (uint32_t u = gl; u < na; u += GL) ls[u] = __ldcg(gss + u);
+            for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + u);
         }
-        __syncwarp(FULL);
-        const uint32_t nA = cnt[0], nB = cnt[1];
         __syncwarp(FULL);
         ph.mark(2);
         A bsc = amax<A>();
@@ -468,7 +486,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         // all (i, i') with i in j*, i' in {NONE} u j'; lexicographic min of (score, i, rank(i'))
         // two j* members per lane and step: every j' member loaded once serves two pairs
         auto ival = [&](uint32_t u, uint32_t& ii, A& se, A& sl, A& pe, A& pl) {
-            const uint32_t pi = u < cap ? (uint32_t)ls[u] : (uint32_t)__ldcg(gss + (u - cap));
+            const uint32_t pi = u < cap ? (uint32_t)ls[u] : (uint32_t)__ldcg(gss + u);
             const Pair2<A> a = T.el(pi);
             ii = T.idx(pi);
             se = Bs.a - a.a;  // j* without i
@@ -519,14 +537,14 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             }
             for (; v < nBs; ++v) pair(lp[v]);
             for (v = cap; v + 4 <= nB; v += 4) {
-                const uint32_t q0 = __ldcg(gsp + (v - cap)), q1 = __ldcg(gsp + (v + 1 - cap));
-                const uint32_t q2 = __ldcg(gsp + (v + 2 - cap)), q3 = __ldcg(gsp + (v + 3 - cap));
+                const uint32_t q0 = __ldcg(gsp + v), q1 = __ldcg(gsp + v + 1);
+                const uint32_t q2 = __ldcg(gsp + v + 2), q3 = __ldcg(gsp + v + 3);
                 pair(q0);
                 pair(q1);
                 pair(q2);
                 pair(q3);
             }
-            for (v = max(v, cap); v < nB; ++v) pair(__ldcg(gsp + (v - cap)));
+            for (v = max(v, cap); v < nB; ++v) pair(__ldcg(gsp + v));
         }
         ph.mark(3);
         if (sizeof(A) == 4) {
@@ -540,26 +558,51 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         } else {
             lexmin_reduce<A, GL>(bsc, bi, brk, FULL);
         }
-        if (apply && gl == 0 && bi != 0xFFFFFFFFu && bsc < Ws) {
+        if (apply && bi != 0xFFFFFFFFu && bsc < Ws) {  // uniform in the group (reduced values)
             const uint32_t pi = __ldg(p.item_pos + bi);
-            const ItemRec<A> a = T.item(pi);
-            const A ae = PK ? (A)((uint32_t)a.e << sh) : a.e, al = PK ? (A)((uint32_t)a.l << sh) : a.l;
-            Pair2<A> es = EL[js], fs = FL[js], ep = EL[jp], fp = FL[jp];
-            es.a -= ae; es.b -= al; fs.a -= a.ef; fs.b -= a.lf;
-            ep.a += ae; ep.b += al; fp.a += a.ef; fp.b += a.lf;
-            set_apos(apos, pi, jp, wide);
-            if (brk != 0u) {
-                const uint32_t pj = __ldg(p.item_pos + (brk - 1u));
-                const ItemRec<A> b = T.item(pj);
-                const A be = PK ? (A)((uint32_t)b.e << sh) : b.e, bl = PK ? (A)((uint32_t)b.l << sh) : b.l;
-                ep.a -= be; ep.b -= bl; fp.a -= b.ef; fp.b -= b.lf;
-                es.a += be; es.b += bl; fs.a += b.ef; fs.b += b.lf;
-                set_apos(apos, pj, js, wide);
+            const uint32_t pj = brk != 0u ? __ldg(p.item_pos + (brk - 1u)) : 0xFFFFFFFFu;
+            // a move adds a member to j': it needs a free entry, else the lists are rebuilt
+            const bool fits = brk != 0u || nB < off[jp + 1] - off[jp];
+            if (fits) {  // i leaves j*'s list (replaced by i', or by the last member)
+                for (uint32_t u = gl; u < nA; u += GL) {
+                    const uint32_t q = u < cap ? (uint32_t)ls[u] : (uint32_t)__ldcg(gss + u);
+                    if (q == pi) {
+                        const uint32_t last = nA - 1u < cap ? (uint32_t)ls[nA - 1u] : (uint32_t)__ldcg(gss + nA - 1u);
+                        gss[u] = (uint16_t)(brk != 0u ? pj : last);
+                    }
+                }
+                if (brk != 0u) {  // i' leaves j''s list, i takes its entry
+                    for (uint32_t v = gl; v < nB; v += GL) {
+                        const uint32_t q = v < cap ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v);
+                        if (q == pj) gsp[v] = (uint16_t)pi;
+                    }
+                } else if (gl == 0) {
+                    gsp[nB] = (uint16_t)pi;
+                    cnt[js] = nA - 1u;
+                    cnt[jp] = nB + 1u;
+                }
+            } else {
+                dirty = true;
             }
-            EL[js] = es;
-            FL[js] = fs;
-            EL[jp] = ep;
-            FL[jp] = fp;
+            if (gl == 0) {
+                const ItemRec<A> a = T.item(pi);
+                const A ae = PK ? (A)((uint32_t)a.e << sh) : a.e, al = PK ? (A)((uint32_t)a.l << sh) : a.l;
+                Pair2<A> es = EL[js], fs = FL[js], ep = EL[jp], fp = FL[jp];
+                es.a -= ae; es.b -= al; fs.a -= a.ef; fs.b -= a.lf;
+                ep.a += ae; ep.b += al; fp.a += a.ef; fp.b += a.lf;
+                set_apos(apos, pi, jp, wide);
+                if (brk != 0u) {
+                    const ItemRec<A> b = T.item(pj);
+                    const A be = PK ? (A)((uint32_t)b.e << sh) : b.e, bl = PK ? (A)((uint32_t)b.l << sh) : b.l;
+                    ep.a -= be; ep.b -= bl; fp.a -= b.ef; fp.b -= b.lf;
+                    es.a += be; es.b += bl; fs.a += b.ef; fs.b += b.lf;
+                    set_apos(apos, pj, js, wide);
+                }
+                EL[js] = es;
+                FL[js] = fs;
+                EL[jp] = ep;
+                FL[jp] = fp;
+            }
         }
         __syncwarp(FULL);
         ph.mark(4);
@@ -621,7 +664,7 @@ DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, c
 
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
-                             Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* spill, uint32_t gl, u64& Tc,
+                             Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, u64& Tc,
                              u64& cmax, PhaseTimer& ph) {
     const uint32_t m = p.m;
     for (uint32_t j = gl; j < m; j += GL) {
@@ -649,7 +692,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
     } else {
         lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, gl);
         ph.mark(0);
-        if (m >= 2) refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, spill, gl, c >= 2, ph);
+        if (m >= 2) refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
     }
     A cm = 0;
     for (uint32_t j = gl; j < m; j += GL) {
@@ -691,7 +734,7 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     uint8_t* scr = base + p.off_scr;
     const uint32_t slot = blockIdx.x * cpb + grp;
     uint8_t* bufs = p.slot_apos + (size_t)slot * 2 * p.apos_bytes;
-    uint16_t* spill = p.slot_spill + (size_t)slot * 2 * (p.n + 512);
+    uint16_t* csr = p.slot_csr + (size_t)slot * p.csr_len;
     // padding past n never matches a bucket (0xFF / 0xFFFF)
     const uint32_t used = p.n * (p.wide ? 2u : 1u);
     for (uint32_t b = used + gl; b < p.apos_bytes; b += GL) {
@@ -708,7 +751,7 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         const uint32_t c = valid ? c0 + grp : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
         u64 Tc, cmax;
-        run_candidate<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, spill, gl, Tc, cmax, ph);
+        run_candidate<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, csr, gl, Tc, cmax, ph);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
         u64 key;
         if (Tc >= (1ull << 40)) {

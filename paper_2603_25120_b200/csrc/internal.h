@@ -63,7 +63,10 @@ struct BalanceShape {
 };
 struct BalanceConfig {
     int gl = 1;                        // lanes per candidate
-    uint32_t cap = 0;                  // refinement list capacity
+    uint32_t cap = 0;                  // refinement: member-list entries copied to shared memory
+    uint32_t sigma = 0;                // refinement: free entries per bucket in the CSR member lists
+    uint32_t csr_len = 0;              // refinement: u16 entries of one slot's CSR lists
+    bool cnt_smem = true;              // refinement: list counters/offsets in shared memory
     uint32_t apos_bytes = 0;           // one assignment buffer (u8 or u16 per position)
     // per kernel variant: [0] packed u32, [1] plain u32, [2] u64 (cand.cuh)
     bool tbl_smem[3] = {false, false, false};  // item table staged in shared memory
@@ -75,7 +78,7 @@ struct BalanceConfig {
     uint32_t n_slots = 0;
     // workspace layout (byte offsets)
     size_t o_hdr, o_keys, o_order, o_item_pos, o_items32, o_items64, o_slot_key, o_slot_T, o_slot_cmax,
-        o_slot_buf, o_slot_apos, o_slot_spill, o_grp, total;
+        o_slot_buf, o_slot_apos, o_slot_csr, o_grp, total;
     bool ok = false;
     std::string why;
 };
