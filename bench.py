@@ -313,7 +313,8 @@ def main():
         "gpu_launches": int(prof["kernel_launches"]),
         "roofline": roofline,
         "clocks": clk.summary(),
-        "winner": {"cand": res["cand"], "makespan_ticks": res["makespan"], "cmax_ticks": res["cmax"]},
+        "winner": {"batch": (args.warmup + args.steps - 1) % n_batches, "cand": res["cand"],
+                   "makespan_ticks": res["makespan"], "cmax_ticks": res["cmax"]},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample, thr = oracle_rate(p, K, args.cpu_seconds)

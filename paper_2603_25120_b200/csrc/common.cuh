@@ -35,30 +35,6 @@ DFLOP_DEV uint32_t mulhi32(uint32_t u, uint32_t n) { return __umulhi(u, n); }
 
 // ---------------------------------------------------------------- fp32 grid (predict)
 // A throughput grid staged in shared memory for the per-sample kernel (R3 interpolation).
-struct GridF {
-    float x[DFLOP_MAX_X];
-    float v[DFLOP_MAX_TP][DFLOP_MAX_X];
-    float tp[DFLOP_MAX_TP];
-    int n_x, n_tp;
-};
-
-DFLOP_DEV float lerp1f(const float* xs, const float* vs, int n, float x) {
-    if (n == 1) return vs[0];
-    float xh = fminf(fmaxf(x, xs[0]), xs[n - 1]);
-    int k = 0;
-    while (k + 1 < n - 1 && xs[k + 1] <= xh) ++k;
-    float w = (xh - xs[k]) / (xs[k + 1] - xs[k]);
-    return (1.0f - w) * vs[k] + w * vs[k + 1];
-}
-
-// interp over (x, tp) with the tp bracket precomputed by the caller (uniform per launch)
-DFLOP_DEV float interp_grid_f(const GridF& g, float x, int a, float wt) {
-    if (g.n_tp == 1) return lerp1f(g.x, g.v[0], g.n_x, x);
-    float r0 = lerp1f(g.x, g.v[a], g.n_x, x);
-    float r1 = lerp1f(g.x, g.v[a + 1], g.n_x, x);
-    return (1.0f - wt) * r0 + wt * r1;
-}
-
 // ---------------------------------------------------------------- candidate state types
 // Per-sample record in LPT base-order position t: combined encoder cost e = ef + eb, LLM
 // cost l = lf + lb, and the forward parts needed by the 1F1B scoring.

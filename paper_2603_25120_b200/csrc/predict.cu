@@ -5,9 +5,11 @@
 //   lf = scale_att * s^2 / L_attn_thr(s, L_tp) + scale_lin * s / L_lin_thr(s, L_tp)
 //   eb = r * ef, lb = r * lf
 // where the host folds 1e9 * FLOPs-per-unit / (tp * pp) / tick (and L_dp / E_dp, R13) into
-// the fp32 scale constants in double precision.  One thread handles 4 consecutive samples
-// with 16-byte loads/stores: 12 B in and 32 B out per sample and plan, HBM-bound at large n.
-// Multi-plan launches (Stage B of the search) use blockIdx.y as the plan index.
+// the fp32 scale constants in double precision, and blends each grid's two TP rows at the
+// plan's TP once (double, then fp32).  Per sample: three binary-searched interpolations, three
+// reciprocals.  One thread handles 4 consecutive samples with 16-byte loads/stores: 12 B in
+// and 32 B out per sample and plan.  Multi-plan launches (Stage B of the search) use
+// blockIdx.y as the plan index.
 #include <algorithm>
 #include <cmath>
 
@@ -16,21 +18,40 @@
 
 namespace dflop {
 
+// Knots of one throughput grid and the reciprocal interval widths (shared by all plans).
+struct PredictKnots {
+    float x[DFLOP_MAX_X];
+    float inv[DFLOP_MAX_X];  // 1 / (x[k+1] - x[k]) (from double)
+    int n_x;
+    int pad;
+};
 struct PredictGrids {
-    GridF e, att, lin;
+    PredictKnots e, att, lin;
 };
-
+// Per plan: the constants and, for each grid, the row blended at the plan's TP (the blend
+// weight is uniform per plan, and interpolation is linear in the row values, so blending the
+// rows once equals blending the two row interpolations of O3 up to rounding).
+struct PredictPlan {
+    PredictConsts c;
+    float ve[DFLOP_MAX_X], va[DFLOP_MAX_X], vl[DFLOP_MAX_X];
+};
+constexpr int kPredictPlans = 16;  // plans per launch (kernel-parameter budget)
 struct PredictLaunch {
-    PredictConsts c[64];
+    PredictPlan pl[kPredictPlans];
 };
 
-DFLOP_DEV void tp_bracket(const GridF& g, float tp, int& a, float& wt) {
-    a = 0;
-    wt = 0.0f;
-    if (g.n_tp == 1) return;
-    const float th = fminf(fmaxf(tp, g.tp[0]), g.tp[g.n_tp - 1]);
-    while (a + 1 < g.n_tp - 1 && g.tp[a + 1] <= th) ++a;
-    wt = (th - g.tp[a]) / (g.tp[a + 1] - g.tp[a]);
+// O3 interp1 on the blended row: clamp, k = largest index with x_k <= x and k <= n-2 (binary
+// search), w = (x - x_k) / (x_{k+1} - x_k), (1 - w) v_k + w v_{k+1} (exact at the knots)
+DFLOP_DEV float interp_row(const PredictKnots& g, const float* v, float x) {
+    const int n = g.n_x;
+    if (n == 1) return v[0];
+    const float xh = fminf(fmaxf(x, g.x[0]), g.x[n - 1]);
+    int k = 0;
+#pragma unroll
+    for (int step = DFLOP_MAX_X / 2; step > 0; step >>= 1)
+        if (k + step <= n - 2 && g.x[k + step] <= xh) k += step;
+    const float w = (xh - g.x[k]) * g.inv[k];
+    return (1.0f - w) * v[k] + w * v[k + 1];
 }
 
 DFLOP_DEV uint32_t to_ticks(float v, uint32_t& ovf) {
@@ -47,15 +68,13 @@ __global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaun
                                                  uint32_t n, float* cost_f32, uint32_t* cost_ticks, size_t plan_stride,
                                                  uint32_t* dev_status) {
     __shared__ PredictGrids g;
+    __shared__ PredictPlan pp;
     for (uint32_t w = threadIdx.x; w < sizeof(PredictGrids) / 4; w += blockDim.x)
         reinterpret_cast<uint32_t*>(&g)[w] = reinterpret_cast<const uint32_t*>(&grids)[w];
+    for (uint32_t w = threadIdx.x; w < sizeof(PredictPlan) / 4; w += blockDim.x)
+        reinterpret_cast<uint32_t*>(&pp)[w] = reinterpret_cast<const uint32_t*>(&L.pl[blockIdx.y])[w];
     __syncthreads();
-    const PredictConsts k = L.c[blockIdx.y];
-    int ae, aa, al;
-    float we, wa, wl;
-    tp_bracket(g.e, k.tp_e, ae, we);
-    tp_bracket(g.att, k.tp_l, aa, wa);
-    tp_bracket(g.lin, k.tp_l, al, wl);
+    const PredictConsts k = pp.c;
     float* f32 = cost_f32 ? cost_f32 + (size_t)blockIdx.y * plan_stride : nullptr;
     uint32_t* tk = cost_ticks ? cost_ticks + (size_t)blockIdx.y * plan_stride : nullptr;
     uint32_t ovf = 0;
@@ -83,9 +102,9 @@ __global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaun
             const float b = (float)((u64)tv[u] + fv[u]);
             const float s = (float)((u64)xv[u] + (u64)k.tau_tile * tv[u] + (u64)k.tau_frame * fv[u]);
             float ef = 0.0f;
-            if (b > 0.0f) ef = (k.scale_e * b) / interp_grid_f(g.e, b, ae, we);
-            const float lf = (k.scale_att * s * s) / interp_grid_f(g.att, s, aa, wa) +
-                             (k.scale_lin * s) / interp_grid_f(g.lin, s, al, wl);
+            if (b > 0.0f) ef = (k.scale_e * b) * __frcp_rn(interp_row(g.e, pp.ve, b));
+            const float lf = (k.scale_att * s * s) * __frcp_rn(interp_row(g.att, pp.va, s)) +
+                             (k.scale_lin * s) * __frcp_rn(interp_row(g.lin, pp.vl, s));
             o[0][u] = ef;
             o[1][u] = k.bwd * ef;
             o[2][u] = lf;
@@ -107,13 +126,33 @@ __global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaun
     if (ovf && dev_status) atomicOr(dev_status, (uint32_t)DFLOP_DEV_COST_OVERFLOW);
 }
 
-static void to_gridf(const dflop_grid& s, GridF& d) {
+static void to_knots(const dflop_grid& s, PredictKnots& d) {
     d.n_x = (int)s.n_x;
-    d.n_tp = (int)s.n_tp;
-    for (int k = 0; k < DFLOP_MAX_X; ++k) d.x[k] = k < (int)s.n_x ? (float)s.x[k] : 0.0f;
-    for (int a = 0; a < DFLOP_MAX_TP; ++a) {
-        d.tp[a] = a < (int)s.n_tp ? (float)s.tp[a] : 0.0f;
-        for (int k = 0; k < DFLOP_MAX_X; ++k) d.v[a][k] = (a < (int)s.n_tp && k < (int)s.n_x) ? (float)s.v[a][k] : 0.0f;
+    d.pad = 0;
+    for (int k = 0; k < DFLOP_MAX_X; ++k) {
+        d.x[k] = k < (int)s.n_x ? (float)s.x[k] : 0.0f;
+        d.inv[k] = k + 1 < (int)s.n_x ? (float)(1.0 / (s.x[k + 1] - s.x[k])) : 0.0f;
+    }
+}
+
+// the grid's row at throughput-TP `tp`: O3's TP bracket (clamp, largest a <= q-2 with
+// t_a <= tp) and weight, applied to the rows in double
+static void blend_row(const dflop_grid& s, double tp, float* out) {
+    int a = 0;
+    double wt = 0.0;
+    if (s.n_tp > 1) {
+        const double th = std::min(std::max(tp, s.tp[0]), s.tp[s.n_tp - 1]);
+        while (a + 1 < (int)s.n_tp - 1 && s.tp[a + 1] <= th) ++a;
+        wt = (th - s.tp[a]) / (s.tp[a + 1] - s.tp[a]);
+    }
+    for (int k = 0; k < DFLOP_MAX_X; ++k) {
+        if (k >= (int)s.n_x) {
+            out[k] = 0.0f;
+        } else if (s.n_tp == 1) {
+            out[k] = (float)s.v[0][k];
+        } else {
+            out[k] = (float)((1.0 - wt) * s.v[a][k] + wt * s.v[a + 1][k]);
+        }
     }
 }
 
@@ -145,9 +184,9 @@ cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* const
                            cudaStream_t s) {
     if (n == 0 || n_plans == 0) return cudaSuccess;
     PredictGrids g;
-    to_gridf(m->thr_e, g.e);
-    to_gridf(m->thr_att, g.att);
-    to_gridf(m->thr_lin, g.lin);
+    to_knots(m->thr_e, g.e);
+    to_knots(m->thr_att, g.att);
+    to_knots(m->thr_lin, g.lin);
     const bool vec = (n % 4 == 0) && ((uintptr_t)tiles % 16 == 0) && ((uintptr_t)frames % 16 == 0) &&
                      ((uintptr_t)text % 16 == 0) && (!cost_f32 || (uintptr_t)cost_f32 % 16 == 0) &&
                      (!cost_ticks || (uintptr_t)cost_ticks % 16 == 0) && (plan_stride % 4 == 0);
@@ -155,10 +194,15 @@ cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* const
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t work = vec ? n / 4 : n;
-    for (uint32_t p0 = 0; p0 < n_plans; p0 += 64) {
-        const uint32_t np = std::min<uint32_t>(64, n_plans - p0);
+    for (uint32_t p0 = 0; p0 < n_plans; p0 += kPredictPlans) {
+        const uint32_t np = std::min<uint32_t>(kPredictPlans, n_plans - p0);
         PredictLaunch L;
-        for (uint32_t i = 0; i < np; ++i) L.c[i] = consts[p0 + i];
+        for (uint32_t i = 0; i < np; ++i) {
+            L.pl[i].c = consts[p0 + i];
+            blend_row(m->thr_e, consts[p0 + i].tp_e, L.pl[i].ve);
+            blend_row(m->thr_att, consts[p0 + i].tp_l, L.pl[i].va);
+            blend_row(m->thr_lin, consts[p0 + i].tp_l, L.pl[i].vl);
+        }
         const uint32_t gx = std::max(1u, std::min<uint32_t>((work + 255) / 256, (uint32_t)sms * 8 / np + 1));
         dim3 grid(gx, np);
         float* f = cost_f32 ? cost_f32 + (size_t)p0 * plan_stride : nullptr;
