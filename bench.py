@@ -294,11 +294,15 @@ def main():
                 "kernel_ms": cand_ms, "kernel_share_of_step": cand_ms / ms_per_step,
                 "peak_note": f"{n_sm} SM x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
                 "ops_per_candidate": algorithmic_ops_per_candidate(p.n, m, S, p.R, p.G)}
+    # traffic: dram__bytes_read.sum + dram__bytes_write.sum of the candidate kernel from the
+    # committed ncu --set full capture (profiles/traffic.json), per candidate x this launch's K
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         tr = json.load(open(traffic_file)).get(p.name)
         if tr:
-            roofline["traffic"] = tr
+            roofline["traffic"] = tr["dram_bytes_per_candidate"] * (e - b)
+            roofline["traffic_unit"] = "B"
+            roofline["traffic_source"] = tr["source"]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -107,7 +107,9 @@ __global__ void k_build_items(const uint32_t* __restrict__ cost, uint32_t n, uin
         const uint32_t ef = cost[i], eb = cost[(size_t)n + i], lf = cost[2 * (size_t)n + i],
                        lb = cost[3 * (size_t)n + i];
         if (fits)
-            it32[t] = ItemRec<uint32_t>{ef + eb, lf + lb, ef, lf};
+            // packed variant: e and l pre-shifted into the key position (E << s | j sums)
+            it32[t] = packed ? ItemRec<uint32_t>{(ef + eb) << sh, (lf + lb) << sh, ef, lf}
+                             : ItemRec<uint32_t>{ef + eb, lf + lb, ef, lf};
         else
             it64[t] = ItemRec<u64>{(u64)ef + eb, (u64)lf + lb, (u64)ef, (u64)lf};
     }

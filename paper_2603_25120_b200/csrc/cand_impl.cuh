@@ -207,6 +207,13 @@ DFLOP_DEV uint64_t batch_perms(uint32_t g0, uint32_t W, uint32_t nc, uint32_t c,
     return perm;
 }
 
+// (hi << 32 | lo) as a register pair, without 64-bit arithmetic
+DFLOP_DEV u64 pack64(uint32_t hi, uint32_t lo) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+    return r;
+}
+
 // ---------------------------------------------------------------- item table access
 template <typename A, bool SM>
 struct Tbl {
@@ -235,6 +242,12 @@ struct Tbl {
 template <typename A, bool PK>
 DFLOP_DEV A unpack(A v, uint32_t sh) {
     return PK ? (A)(v >> sh) : v;
+}
+// the same load kept in the shifted domain (W << s) of the packed variant, whose item records
+// hold e << s and l << s (k_build_items): comparisons and differences are unchanged
+template <typename A, bool PK>
+DFLOP_DEV A keyval(A v, uint32_t sh) {
+    return PK ? (A)(v & ~((1u << sh) - 1u)) : v;
 }
 
 DFLOP_DEV void set_apos(uint8_t* apos, uint32_t pos, uint32_t j, bool wide) {
@@ -347,7 +360,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
             uint32_t bj;
             if (PK) {
                 // keys (W << s) | j: one fused add-max and one min per probe
-                const uint32_t es = ((uint32_t)it.e << sh) & (uint32_t)use, ls = ((uint32_t)it.l << sh) & (uint32_t)use;
+                const uint32_t es = (uint32_t)it.e & (uint32_t)use, ls = (uint32_t)it.l & (uint32_t)use;
                 uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
                 if (m == 8 * GL) {  // every preset: exactly 8 buckets per lane, no bounds tests
                     probe_fixed<8, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, es, ls, b0, b1);
@@ -404,8 +417,8 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
             // update needs no warp barrier (the shuffles already order the lanes)
             if ((bj & (GL - 1)) == gl) {
                 Pair2<A> el = EL[bj], fl = FL[bj];
-                el.a += PK ? (A)((uint32_t)it.e << sh) : it.e;
-                el.b += PK ? (A)((uint32_t)it.l << sh) : it.l;
+                el.a += it.e;
+                el.b += it.l;
                 fl.a += it.ef;
                 fl.b += it.lf;
                 EL[bj] = el;
@@ -452,7 +465,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         uint32_t jb = 0xFFFFFFFFu;
         for (uint32_t j = gl; j < m; j += GL) {
             const Pair2<A> el = EL[j];
-            const A W = unpack<A, PK>(maxa(el.a, el.b), sh);
+            const A W = keyval<A, PK>(maxa(el.a, el.b), sh);
             if (jb == 0xFFFFFFFFu || W > Wb) {
                 Wb = W;
                 jb = j;
@@ -464,8 +477,8 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         const Philox4 w = philox4x32_10(r, c, 1u, 0u, p.seed0, p.seed1);
         const uint32_t jp = (js + 1u + mulhi32(w.x, m - 1u)) % m;
         const Pair2<A> Bsp = EL[js], Bpp = EL[jp];
-        const Pair2<A> Bs{unpack<A, PK>(Bsp.a, sh), unpack<A, PK>(Bsp.b, sh)};
-        const Pair2<A> Bp{unpack<A, PK>(Bpp.a, sh), unpack<A, PK>(Bpp.b, sh)};
+        const Pair2<A> Bs{keyval<A, PK>(Bsp.a, sh), keyval<A, PK>(Bsp.b, sh)};
+        const Pair2<A> Bp{keyval<A, PK>(Bpp.a, sh), keyval<A, PK>(Bpp.b, sh)};
         ph.mark(1);
         // member lists of j* (gss) and j' (gsp); their first cap entries are copied to
         // shared memory (ls, lp), the rest is read from L2
@@ -481,7 +494,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         ph.mark(2);
         A bsc = amax<A>();
         uint32_t bi = 0xFFFFFFFFu, brk = 0xFFFFFFFFu;
-        u64 bkey = ~0ull;  // 32-bit scores: (score << 32 | item << 16 | rank), a branch-free min
+        u64 bkey = ~0ull;  // 32-bit scores: (score << 32 | item << 16 | rank), branch-free minima
         const uint32_t nBs = min(nB, cap);
         // all (i, i') with i in j*, i' in {NONE} u j'; lexicographic min of (score, i, rank(i'))
         // two j* members per lane and step: every j' member loaded once serves two pairs
@@ -508,10 +521,10 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 pl1 = pl0;
             }
             const A n0 = maxa(maxa(se0, sl0), maxa(pe0, pl0)), n1 = maxa(maxa(se1, sl1), maxa(pe1, pl1));
-            const u64 h0 = (u64)i0 << 16, h1 = (u64)i1 << 16;
-            if (sizeof(A) == 4) {
-                bkey = min(bkey, min(((u64)n0 << 32) | h0, ((u64)n1 << 32) | h1));
-            } else {
+            // 32-bit scores: per row the minimum of (score << 32 | rank) (rank 0 = NONE), the
+            // item index is or-ed in once per row below
+            u64 r0 = (u64)n0 << 32, r1 = (u64)n1 << 32;
+            if (sizeof(A) != 4) {
                 lex_update(bsc, bi, brk, n0, i0, 0u);
                 lex_update(bsc, bi, brk, n1, i1, 0u);
             }
@@ -521,7 +534,8 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 const A s0 = maxa(maxa<A>(se0 + b.a, sl0 + b.b), maxa<A>(pe0 - b.a, pl0 - b.b));
                 const A s1 = maxa(maxa<A>(se1 + b.a, sl1 + b.b), maxa<A>(pe1 - b.a, pl1 - b.b));
                 if (sizeof(A) == 4) {
-                    bkey = min(bkey, min(((u64)s0 << 32) | h0 | rk, ((u64)s1 << 32) | h1 | rk));
+                    r0 = min(r0, pack64((uint32_t)s0, rk));
+                    r1 = min(r1, pack64((uint32_t)s1, rk));
                 } else {
                     lex_update(bsc, bi, brk, s0, i0, rk);
                     lex_update(bsc, bi, brk, s1, i1, rk);
@@ -545,6 +559,8 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 pair(q3);
             }
             for (v = max(v, cap); v < nB; ++v) pair(__ldcg(gsp + v));
+            if (sizeof(A) == 4)  // (score, item, rank): the rank field is 16 bits (n <= 65535)
+                bkey = min(bkey, min(r0 | ((u64)i0 << 16), r1 | ((u64)i1 << 16)));
         }
         ph.mark(3);
         if (sizeof(A) == 4) {
@@ -586,14 +602,14 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             }
             if (gl == 0) {
                 const ItemRec<A> a = T.item(pi);
-                const A ae = PK ? (A)((uint32_t)a.e << sh) : a.e, al = PK ? (A)((uint32_t)a.l << sh) : a.l;
+                const A ae = a.e, al = a.l;
                 Pair2<A> es = EL[js], fs = FL[js], ep = EL[jp], fp = FL[jp];
                 es.a -= ae; es.b -= al; fs.a -= a.ef; fs.b -= a.lf;
                 ep.a += ae; ep.b += al; fp.a += a.ef; fp.b += a.lf;
                 set_apos(apos, pi, jp, wide);
                 if (brk != 0u) {
                     const ItemRec<A> b = T.item(pj);
-                    const A be = PK ? (A)((uint32_t)b.e << sh) : b.e, bl = PK ? (A)((uint32_t)b.l << sh) : b.l;
+                    const A be = b.e, bl = b.l;
                     ep.a -= be; ep.b -= bl; fp.a -= b.ef; fp.b -= b.lf;
                     es.a += be; es.b += bl; fs.a += b.ef; fs.b += b.lf;
                     set_apos(apos, pj, js, wide);
