@@ -133,8 +133,24 @@ static int round_ticks(double x_ns, double tick_ns, uint32_t* q) {
     return ORC_OK;
 }
 
+/* N1 shape bin (R30): floor(log2 x) by repeated halving; x = 0 is bin 0; clamped. */
+uint32_t orc_shape_bin(uint64_t x) {
+    uint32_t q = 0;
+    while (x >= 2) {
+        x /= 2;
+        q++;
+    }
+    return q < ORC_CORR_BINS ? q : ORC_CORR_BINS - 1;
+}
+
 int orc_predict(const orc_model* m, const orc_plan* p, const uint32_t* tiles, const uint32_t* frames,
                 const uint32_t* text, uint32_t n, double* cost_f64, uint32_t* cost_q, uint32_t* bad) {
+    return orc_predict_corrected(m, p, tiles, frames, text, n, NULL, cost_f64, cost_q, bad);
+}
+
+int orc_predict_corrected(const orc_model* m, const orc_plan* p, const uint32_t* tiles, const uint32_t* frames,
+                          const uint32_t* text, uint32_t n, const double* rho, double* cost_f64, uint32_t* cost_q,
+                          uint32_t* bad) {
     double lin_e = 24.0 * (double)m->e_hidden * (double)m->e_hidden;
     double att_e = m->e_attn ? 4.0 * (double)m->e_hidden : 0.0;
     double per_inst_e = lin_e * (double)m->e_seq + att_e * (double)m->e_seq * (double)m->e_seq;
@@ -152,12 +168,17 @@ int orc_predict(const orc_model* m, const orc_plan* p, const uint32_t* tiles, co
         if (b > 0) {
             double EF = bd * c_e;
             double thr = orc_interp_thr(&m->thr_e, bd, (double)p->e_tp);
+            if (rho) thr = thr * rho[0 * ORC_CORR_BINS + orc_shape_bin(b)]; /* N1: corrected */
             ef = 1e9 * EF / (thr * (double)p->e_tp * (double)p->e_pp) * ((double)p->l_dp / (double)p->e_dp);
         }
         double Llin = c_lin * sd;
         double Latt = c_att * sd * sd;
         double thr_a = orc_interp_thr(&m->thr_att, sd, (double)p->l_tp);
         double thr_l = orc_interp_thr(&m->thr_lin, sd, (double)p->l_tp);
+        if (rho) { /* N1: corrected throughput of the sample's shape bin */
+            thr_a = thr_a * rho[1 * ORC_CORR_BINS + orc_shape_bin(s)];
+            thr_l = thr_l * rho[2 * ORC_CORR_BINS + orc_shape_bin(s)];
+        }
         double lf = 1e9 * (Latt / thr_a + Llin / thr_l) / ((double)p->l_tp * (double)p->l_pp);
         double eb = m->bwd_ratio * ef;
         double lb = m->bwd_ratio * lf;

@@ -100,6 +100,19 @@ double orc_interp_mem(const orc_mgrid* g, double l, double tp, double x);
 int orc_predict(const orc_model* m, const orc_plan* p, const uint32_t* tiles, const uint32_t* frames,
                 const uint32_t* text, uint32_t n, double* cost_f64, uint32_t* cost_q, uint32_t* bad);
 
+/* N1 Adaptive Correction (Eq. (6) B = Th_actual - Th_pred; S:374-377,
+ * S:383-386): rho[g][q] = Th_actual / Th_pred for throughput grid g (0 = E_thr on b,
+ * 1 = L_attn_thr on s, 2 = L_lin_thr on s) and shape bin q = floor(log2 x) (x = 0 -> 0,
+ * clamped to ORC_CORR_BINS - 1) (R30).  With rho != NULL the predicted throughput of a
+ * sample is replaced by the corrected one, Th_pred * rho ("predictions for
+ * shape-buckets with recorded deviations are replaced by the corrected throughput");
+ * rho == NULL is orc_predict. */
+#define ORC_CORR_BINS 32
+uint32_t orc_shape_bin(uint64_t x);
+int orc_predict_corrected(const orc_model* m, const orc_plan* p, const uint32_t* tiles, const uint32_t* frames,
+                          const uint32_t* text, uint32_t n, const double* rho, double* cost_f64, uint32_t* cost_q,
+                          uint32_t* bad);
+
 /* Step a2: base order pi: key max(e_i, l_i) descending, index ascending. */
 void orc_base_order(const uint32_t* cost_q, uint32_t n, uint32_t* order);
 

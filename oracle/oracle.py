@@ -84,6 +84,10 @@ def lib():
         L.orc_interp_mem.argtypes = [P(OrcMGrid), C.c_double, C.c_double, C.c_double]
         L.orc_interp_mem.restype = C.c_double
         L.orc_predict.argtypes = [P(OrcModel), P(OrcPlan), u32p, u32p, u32p, C.c_uint32, f64p, u32p, u32p]
+        L.orc_predict_corrected.argtypes = [P(OrcModel), P(OrcPlan), u32p, u32p, u32p, C.c_uint32, f64p, f64p,
+                                            u32p, u32p]
+        L.orc_shape_bin.argtypes = [C.c_uint64]
+        L.orc_shape_bin.restype = C.c_uint32
         L.orc_base_order.argtypes = [u32p, C.c_uint32, u32p]
         L.orc_simulate_1f1b.argtypes = [u64p, u64p, C.c_uint32, C.c_uint32, u64p, u64p]
         L.orc_run_candidate.argtypes = [u32p, C.c_uint32, P(OrcPlan), P(OrcBParams), u32p, C.c_uint32,
@@ -207,6 +211,28 @@ def predict(model: Dict, plan: Dict, tiles, frames, text):
     ms, ps = model_struct(model), plan_struct(plan)
     st = lib().orc_predict(C.byref(ms), C.byref(ps), _p(t, C.c_uint32), _p(f, C.c_uint32), _p(x, C.c_uint32),
                            n, _p(cf64, C.c_double), _p(cq, C.c_uint32), _p(bad, C.c_uint32))
+    return cf64, cq, st, int(bad[0])
+
+
+CORR_BINS = 32
+
+
+def shape_bin(x: int) -> int:
+    return int(lib().orc_shape_bin(C.c_uint64(int(x))))
+
+
+def predict_corrected(model: Dict, plan: Dict, tiles, frames, text, rho):
+    """a1 with Adaptive Correction ratios rho[3][32] (N1); rho=None is predict()."""
+    t, f, x = _u32(tiles), _u32(frames), _u32(text)
+    n = len(t)
+    cf64 = np.zeros((4, n), np.float64)
+    cq = np.zeros((4, n), np.uint32)
+    bad = np.zeros(1, np.uint32)
+    ms, ps = model_struct(model), plan_struct(plan)
+    r = None if rho is None else np.ascontiguousarray(np.asarray(rho, np.float64).reshape(3, CORR_BINS))
+    st = lib().orc_predict_corrected(C.byref(ms), C.byref(ps), _p(t, C.c_uint32), _p(f, C.c_uint32),
+                                     _p(x, C.c_uint32), n, None if r is None else _p(r, C.c_double),
+                                     _p(cf64, C.c_double), _p(cq, C.c_uint32), _p(bad, C.c_uint32))
     return cf64, cq, st, int(bad[0])
 
 

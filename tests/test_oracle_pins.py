@@ -484,3 +484,63 @@ def test_batch_means(O, presets):
     b = t.astype(np.int64) + f
     s = x.astype(np.int64) + p.model["tau_tile"] * t.astype(np.int64) + p.model["tau_frame"] * f.astype(np.int64)
     assert mb == b.sum() / len(b) and ms == s.sum() / len(s)
+
+
+# ------------------------------------------------------------------ N1 Adaptive Correction
+def test_shape_bin_is_floor_log2(O):
+    # R30: q = floor(log2 x), x = 0 -> 0, clamped to 31; Python's int.bit_length is the reference
+    for x in [0, 1, 2, 3, 4, 5, 7, 8, 255, 256, 1023, 1024, 1025, (1 << 20) + 1, (1 << 31) - 1, 1 << 31,
+              (1 << 40) + 7, (1 << 63)]:
+        want = 0 if x == 0 else min(31, x.bit_length() - 1)
+        assert O.shape_bin(x) == want, x
+
+
+def test_correction_halved_throughput_doubles_duration(O, presets):
+    # S:386 "tracker holding a -50% throughput correction for one shape -> that item's
+    # duration doubles"; the other shapes are untouched (bitwise)
+    p = presets[3]
+    t, f, x = p.features(0)
+    base, _, st, _ = O.predict(p.model, p.plan, t, f, x)
+    assert st == 0
+    b = t.astype(np.uint64) + f
+    qb = O.shape_bin(int(b[np.argmax(b)]))
+    rho = np.ones((3, O.CORR_BINS))
+    rho[0, qb] = 0.5
+    cf, _, st, _ = O.predict_corrected(p.model, p.plan, t, f, x, rho)
+    hit = np.array([bb > 0 and O.shape_bin(int(bb)) == qb for bb in b])
+    assert hit.any() and not hit.all()
+    np.testing.assert_allclose(cf[0, hit], 2 * base[0, hit], rtol=1e-15)
+    np.testing.assert_allclose(cf[1, hit], 2 * base[1, hit], rtol=1e-15)
+    assert (cf[0, ~hit] == base[0, ~hit]).all() and (cf[2:] == base[2:]).all()
+
+
+def test_correction_identity_and_grid_separation(O, presets):
+    p = presets[5]
+    t, f, x = p.features(1)
+    base, q0, _, _ = O.predict(p.model, p.plan, t, f, x)
+    cf, q, _, _ = O.predict_corrected(p.model, p.plan, t, f, x, np.ones((3, O.CORR_BINS)))
+    assert (cf == base).all() and (q == q0).all()                 # Eq. (6) B = 0: no correction
+    # both LLM grids corrected by r in every bin: the LLM time scales by exactly 1/r, the
+    # encoder is untouched; the encoder grid alone: only ef, eb change
+    r = 1.25
+    rho = np.ones((3, O.CORR_BINS)); rho[1:] = r
+    cf, _, _, _ = O.predict_corrected(p.model, p.plan, t, f, x, rho)
+    np.testing.assert_allclose(cf[2:], base[2:] / r, rtol=1e-14)
+    assert (cf[:2] == base[:2]).all()
+    rho = np.ones((3, O.CORR_BINS)); rho[0] = 0.8
+    cf, _, _, _ = O.predict_corrected(p.model, p.plan, t, f, x, rho)
+    np.testing.assert_allclose(cf[:2], base[:2] / 0.8, rtol=1e-14)
+    assert (cf[2:] == base[2:]).all()
+
+
+def test_correction_attention_and_linear_bins_separate(O):
+    # a constant-throughput model: lf = 1e9 (4 s^2 / thr_att + 24 s / thr_lin); halving the
+    # attention throughput of s's bin doubles only the attention term (S:243 split)
+    m = unit_model()
+    t, f, x = [0, 0], [0, 0], [5, 100]
+    base, _, _, _ = O.predict(m, plan(), t, f, x)
+    rho = np.ones((3, O.CORR_BINS)); rho[1, O.shape_bin(100)] = 0.5
+    cf, _, _, _ = O.predict_corrected(m, plan(), t, f, x, rho)
+    att, lin = 4.0 * 100 * 100, 24.0 * 100
+    assert abs(cf[2, 1] - (2 * att + lin)) < 1e-6 and abs(base[2, 1] - (att + lin)) < 1e-6
+    assert cf[2, 0] == base[2, 0]
