@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DFLOP_ABI_VERSION 1u
+#define DFLOP_ABI_VERSION 2u
 
 typedef int32_t dflop_status;
 #define DFLOP_OK 0
@@ -84,6 +84,20 @@ typedef struct dflop_mem_grid {
     double v[2][DFLOP_MAX_TP][DFLOP_MAX_X];
 } dflop_mem_grid;
 
+/* Adaptive Correction (N1; Eq. (6) B = Th_actual - Th_pred).
+ * rho[g][q] = Th_actual / Th_pred (the host tracker's exponential average) for throughput
+ * grid g (0 = thr_e on the encoder batch b, 1 = thr_att and 2 = thr_lin on the LLM length s)
+ * and shape bin q = floor(log2 x) (x = 0 -> 0, clamped to DFLOP_CORR_BINS - 1) (R30).  When
+ * `active`, a1 divides each sample's FLOPs by Th_pred * rho instead of Th_pred; a
+ * bin with rho = 1 is unchanged.  rho must be finite and > 0.  Host memory, read during the
+ * call only. */
+#define DFLOP_CORR_BINS 32
+typedef struct dflop_correction {
+    uint32_t struct_size;
+    uint32_t active;                    /* 0: ignored (the cost-benefit rule switched it off) */
+    float rho[3][DFLOP_CORR_BINS];
+} dflop_correction;
+
 /* The MLLM cost model (Table 1 symbols; FLOP accounting R1). */
 typedef struct dflop_cost_model {
     uint32_t struct_size;
@@ -101,6 +115,8 @@ typedef struct dflop_cost_model {
     dflop_grid thr_e;    /* E_thr(b, E_tp)                                      */
     dflop_grid thr_att;  /* L_attn_thr(s, L_tp)                                 */
     dflop_grid thr_lin;  /* L_lin_thr(s, L_tp)                                  */
+    const dflop_correction* correction; /* N1, NULL = none; used by a1 (predict and the
+                                            search's Stage B), not by Stage A (R31)    */
 } dflop_cost_model;
 
 /* Memory model for Eq. (4)-(5). */

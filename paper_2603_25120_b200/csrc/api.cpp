@@ -95,6 +95,14 @@ dflop_status validate_cost_model(const dflop_cost_model* m) {
     if ((st = validate_grid(m->thr_e, "thr_e")) != DFLOP_OK) return st;
     if ((st = validate_grid(m->thr_att, "thr_att")) != DFLOP_OK) return st;
     if ((st = validate_grid(m->thr_lin, "thr_lin")) != DFLOP_OK) return st;
+    if (const dflop_correction* c = m->correction) {
+        if (c->struct_size != sizeof(dflop_correction))
+            return invalid("dflop_correction.struct_size=%u, expected %zu", c->struct_size, sizeof(dflop_correction));
+        for (int g = 0; g < 3; ++g)
+            for (int q = 0; q < DFLOP_CORR_BINS; ++q)
+                if (!(c->rho[g][q] > 0.0f) || !std::isfinite(c->rho[g][q]))
+                    return invalid("correction rho[%d][%d] must be finite and > 0", g, q);
+    }
     return DFLOP_OK;
 }
 

@@ -27,7 +27,16 @@ struct PredictKnots {
 };
 struct PredictGrids {
     PredictKnots e, att, lin;
+    float rho[3][DFLOP_CORR_BINS];  // N1 Adaptive Correction ratios (all 1 when inactive)
+    int corr;                       // correction active
+    int pad[3];
 };
+
+// N1 shape bin: floor(log2 x) from the integer shape, x = 0 -> 0, clamped (R30)
+DFLOP_DEV uint32_t shape_bin(u64 x) {
+    const uint32_t q = x ? 63u - (uint32_t)__clzll((long long)x) : 0u;
+    return q < DFLOP_CORR_BINS ? q : DFLOP_CORR_BINS - 1;
+}
 // Per plan: the constants and, for each grid, the row blended at the plan's TP (the blend
 // weight is uniform per plan, and interpolation is linear in the row values, so blending the
 // rows once equals blending the two row interpolations of O3 up to rounding).
@@ -99,12 +108,19 @@ __global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaun
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (u >= cnt) break;
-            const float b = (float)((u64)tv[u] + fv[u]);
-            const float s = (float)((u64)xv[u] + (u64)k.tau_tile * tv[u] + (u64)k.tau_frame * fv[u]);
+            const u64 bi = (u64)tv[u] + fv[u];
+            const u64 si = (u64)xv[u] + (u64)k.tau_tile * tv[u] + (u64)k.tau_frame * fv[u];
+            const float b = (float)bi, s = (float)si;
+            float te = interp_row(g.e, pp.ve, b), ta = interp_row(g.att, pp.va, s), tl = interp_row(g.lin, pp.vl, s);
+            if (g.corr) {  // N1: corrected throughput of the sample's shape bins (one lookup each)
+                const uint32_t qb = shape_bin(bi), qs = shape_bin(si);
+                te *= g.rho[0][qb];
+                ta *= g.rho[1][qs];
+                tl *= g.rho[2][qs];
+            }
             float ef = 0.0f;
-            if (b > 0.0f) ef = (k.scale_e * b) * __frcp_rn(interp_row(g.e, pp.ve, b));
-            const float lf = (k.scale_att * s * s) * __frcp_rn(interp_row(g.att, pp.va, s)) +
-                             (k.scale_lin * s) * __frcp_rn(interp_row(g.lin, pp.vl, s));
+            if (b > 0.0f) ef = (k.scale_e * b) * __frcp_rn(te);
+            const float lf = (k.scale_att * s * s) * __frcp_rn(ta) + (k.scale_lin * s) * __frcp_rn(tl);
             o[0][u] = ef;
             o[1][u] = k.bwd * ef;
             o[2][u] = lf;
@@ -187,6 +203,10 @@ cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* const
     to_knots(m->thr_e, g.e);
     to_knots(m->thr_att, g.att);
     to_knots(m->thr_lin, g.lin);
+    g.corr = (m->correction && m->correction->active) ? 1 : 0;
+    for (int q = 0; q < 3; ++q)
+        for (int k = 0; k < DFLOP_CORR_BINS; ++k) g.rho[q][k] = g.corr ? m->correction->rho[q][k] : 1.0f;
+    g.pad[0] = g.pad[1] = g.pad[2] = 0;
     const bool vec = (n % 4 == 0) && ((uintptr_t)tiles % 16 == 0) && ((uintptr_t)frames % 16 == 0) &&
                      ((uintptr_t)text % 16 == 0) && (!cost_f32 || (uintptr_t)cost_f32 % 16 == 0) &&
                      (!cost_ticks || (uintptr_t)cost_ticks % 16 == 0) && (plan_stride % 4 == 0);

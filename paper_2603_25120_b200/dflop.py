@@ -44,12 +44,20 @@ class MemGrid(C.Structure):
                 ("x", C.c_double * MAX_X), ("v", ((C.c_double * MAX_X) * MAX_TP) * 2)]
 
 
+CORR_BINS = 32
+
+
+class Correction(C.Structure):
+    """dflop_correction (N1 Adaptive Correction): rho[3][32] = Th_actual / Th_pred."""
+    _fields_ = [("struct_size", C.c_uint32), ("active", C.c_uint32), ("rho", (C.c_float * CORR_BINS) * 3)]
+
+
 class CostModel(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("e_layers", C.c_uint32), ("e_hidden", C.c_uint32),
                 ("e_seq", C.c_uint32), ("e_attn", C.c_uint32), ("l_layers", C.c_uint32), ("l_hidden", C.c_uint32),
                 ("tau_tile", C.c_uint32), ("tau_frame", C.c_uint32), ("reserved", C.c_uint32),
                 ("bwd_ratio", C.c_double), ("tick_ns", C.c_double), ("thr_e", Grid), ("thr_att", Grid),
-                ("thr_lin", Grid)]
+                ("thr_lin", Grid), ("correction", C.POINTER(Correction))]
 
 
 class MemModel(C.Structure):
@@ -173,6 +181,17 @@ def cost_model_struct(m: Dict) -> CostModel:
         setattr(s, k, int(m[k]))
     s.bwd_ratio, s.tick_ns = float(m["bwd_ratio"]), float(m["tick_ns"])
     s.thr_e, s.thr_att, s.thr_lin = grid_struct(m["thr_e"]), grid_struct(m["thr_att"]), grid_struct(m["thr_lin"])
+    corr = m.get("correction")
+    if corr is not None:  # {"active": bool, "rho": [3][32]} (N1), e.g. CorrectionTracker.table()
+        c = Correction()
+        c.struct_size = C.sizeof(Correction)
+        c.active = 1 if corr.get("active", True) else 0
+        rho = corr["rho"]
+        for g in range(3):
+            for q in range(CORR_BINS):
+                c.rho[g][q] = float(rho[g][q])
+        s._corr_keepalive = c          # the pointer below must outlive the call
+        s.correction = C.pointer(c)
     return s
 
 

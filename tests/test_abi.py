@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(D):
 
 
 def test_abi_version_and_last_error(D):
-    assert D.abi_version() == 1
+    assert D.abi_version() == 2
     assert D.lib().dflop_last_error() == b""
 
 
@@ -63,7 +63,9 @@ PROBE = r"""
 int main(void) {
   S(dflop_grid) S(dflop_mem_grid) S(dflop_cost_model) S(dflop_mem_model) S(dflop_plan) S(dflop_cluster)
   S(dflop_balance_params) S(dflop_cand_result) S(dflop_search_params) S(dflop_plan_result) S(dflop_profile)
+  S(dflop_correction) F(dflop_correction, rho)
   F(dflop_cost_model, bwd_ratio) F(dflop_cost_model, thr_e) F(dflop_cost_model, thr_lin)
+  F(dflop_cost_model, correction)
   F(dflop_mem_model, ms_e) F(dflop_mem_model, mem_per_gpu) F(dflop_balance_params, id_base)
   F(dflop_search_params, fixed_plan) F(dflop_search_params, seed) F(dflop_plan_result, makespan)
   F(dflop_plan_result, alg1_plan) F(dflop_plan_result, alg1_makespan) F(dflop_plan_result, n_candidates)
@@ -81,7 +83,8 @@ def test_struct_layouts_match_header(D, tmp_path):
     m = {"dflop_grid": D.Grid, "dflop_mem_grid": D.MemGrid, "dflop_cost_model": D.CostModel,
          "dflop_mem_model": D.MemModel, "dflop_plan": D.Plan, "dflop_cluster": D.Cluster,
          "dflop_balance_params": D.BalanceParams, "dflop_cand_result": D.CandResult,
-         "dflop_search_params": D.SearchParams, "dflop_plan_result": D.PlanResult, "dflop_profile": D.Profile}
+         "dflop_search_params": D.SearchParams, "dflop_plan_result": D.PlanResult, "dflop_profile": D.Profile,
+         "dflop_correction": D.Correction}
     for k, v in got.items():
         if "." in k:
             s, f = k.split(".")
