@@ -413,3 +413,22 @@ def search(model: Dict, mem: Dict, cluster: Dict, tiles, frames, text, gbs, top_
     out["top_pairs"] = np.asarray(top_pairs, np.uint64)
     out["T_A_all"] = T_A
     return out
+
+
+def expected_makespan_choice(plans, batch_costs, K, R, G, seed, threads=None):
+    """N2, Eq. (1): for each plan (in Stage-A rank order) the sum over the sample's
+    batches of T_B(b) -- the batch's best candidate makespan, batch b's family keyed
+    (seed[0], seed[1] + b) (R33) -- and theta* = argmin (sum, rank).  batch_costs[p][b] is
+    the [4][n_b] tick array of plan p on batch b.  Returns (winner rank, sums, per-batch
+    results of every plan)."""
+    sums, per = [], []
+    for p, plan in enumerate(plans):
+        tot, rows = 0, []
+        for b, q in enumerate(batch_costs[p]):
+            r = balance_threaded(q, plan, K, R, G, (seed[0], seed[1] + b), threads=threads, per_candidate=False)
+            tot += int(r["T"])
+            rows.append(r)
+        sums.append(tot)
+        per.append(rows)
+    win = min(range(len(plans)), key=lambda p: (sums[p], p))
+    return win, sums, per

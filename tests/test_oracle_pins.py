@@ -544,3 +544,37 @@ def test_correction_attention_and_linear_bins_separate(O):
     att, lin = 4.0 * 100 * 100, 24.0 * 100
     assert abs(cf[2, 1] - (2 * att + lin)) < 1e-6 and abs(base[2, 1] - (att + lin)) < 1e-6
     assert cf[2, 0] == base[2, 0]
+
+
+# ------------------------------------------------------------------ N2 Eq. (1) over a sample
+def test_expected_makespan_closed_form(O):
+    # uniform items with e = l on every stage: each batch balances perfectly (k items per
+    # bucket), so T_B = (N_mb + S - 1) * k * (f + b) (1F1B closed form, pinned above); the
+    # Eq. (1) objective is the sum over the batches ("sample of two items with T 10
+    # and 20 -> 15", here as sums) and D identical batches give D x T_B
+    pl = plan(e_pp=1, l_pp=2, n_mb=4)
+    m, S = 4, 3
+    def batch(k, f=3, b=6):
+        c = np.zeros((4, m * k), np.uint32)
+        c[0], c[1], c[2], c[3] = f, b, f, b
+        return c
+    ks = [1, 2, 5]
+    win, sums, per = O.expected_makespan_choice([pl], [[batch(k) for k in ks]], 64, 4, 8, (1, 10))
+    want = [(4 + S - 1) * k * 9 for k in ks]
+    assert [int(r["T"]) for r in per[0]] == want and sums[0] == sum(want)
+    _, sums2, _ = O.expected_makespan_choice([pl], [[batch(2)] * 3], 64, 4, 8, (1, 10))
+    assert sums2[0] == 3 * want[1]
+
+
+def test_expected_makespan_argmin_and_ties(O):
+    # two plans: the smaller sum wins; equal sums -> the lower Stage-A rank (R18, R33)
+    a = plan(e_pp=1, l_pp=1, n_mb=2)
+    c = np.zeros((4, 4), np.uint32)
+    c[0], c[2] = [5, 4, 3, 2], [1, 1, 1, 1]
+    win, sums, _ = O.expected_makespan_choice([a, a], [[c, c], [c, c]], 16, 2, 8, (3, 0))
+    assert sums[0] == sums[1] and win == 0
+    b = plan(e_pp=1, l_pp=1, n_mb=4)
+    win, sums, _ = O.expected_makespan_choice([a, b], [[c, c], [c, c]], 16, 2, 8, (3, 0))
+    assert win == min(range(2), key=lambda p: (sums[p], p))
+    # brute force over the sums
+    assert sums[win] == min(sums)
