@@ -329,6 +329,33 @@ dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_cost_model*
                                 dflop_plan_result* out, uint32_t* assign, uint64_t* stage_a_out,
                                 uint64_t stage_a_cap, dflop_stream_t stream);
 
+/* ---------------------------------------------------------------- N2 search over a sample
+ * Eq. (1): theta* = argmin_theta (1/|D|) sum_{d in D} T(d; theta) over a sample
+ * of D global batches, each balanced and scored on the device exactly as in
+ * dflop_search_plans; T(d; theta) = T_B, the batch's best candidate makespan (R33).
+ *   tiles/frames/text  device u32 [batch_offsets[D] - batch_offsets[0]]: the batches
+ *                  back to back; batch b = [batch_offsets[b], batch_offsets[b+1]) (host
+ *                  u32 [D+1], non-decreasing, each batch <= 65535 samples), 1 <= D <= 4096.
+ *   sp             as for dflop_search_plans; batch b's candidate family uses Philox key
+ *                  (seed[0], seed[1] + b).  ALG1: Stage A on the mean shapes of the whole
+ *                  sample (GBS = sp->gbs), Stage B over every (top-P plan, batch).
+ *   out            host: the plan minimising (sum_b T_B(b), Stage-A rank); out->makespan =
+ *                  sum_b T_B(b) (D x the Eq. (1) objective, ticks); cand/cmax/owner_rank
+ *                  are batch 0's.
+ *   batch_results  host dflop_cand_result[D] or NULL: theta*'s winner per batch.
+ *   plan_objective host u64[top_p] or NULL: sum_b T_B(b) per Stage-B plan (Stage-A rank
+ *                  order; UINT64_MAX when a plan had no candidate).
+ *   assign         device u32 [total] or NULL: every batch's winning assignment.
+ * Multi-GPU: candidates sharded as in dflop_search_plans; one NCCL min all-reduce of the
+ * [P x D] key array, then one broadcast per batch from its winner's owner.  Errors as
+ * dflop_search_plans, plus INVALID_ARGUMENT for bad offsets / D. */
+dflop_status dflop_search_plans_batches(const dflop_cluster* cl, const dflop_cost_model* cm,
+                                        const dflop_mem_model* mm, const uint32_t* tiles, const uint32_t* frames,
+                                        const uint32_t* text, const uint32_t* batch_offsets, uint32_t n_batches,
+                                        const dflop_search_params* sp, dflop_comm* comm, void* ws, size_t* ws_bytes,
+                                        dflop_plan_result* out, dflop_cand_result* batch_results,
+                                        uint64_t* plan_objective, uint32_t* assign, dflop_stream_t stream);
+
 /* ---------------------------------------------------------------- NCCL
  * Bootstrap: rank 0 calls dflop_get_unique_id, the caller broadcasts the 128 bytes
  * (e.g. with torch.distributed), then every rank calls dflop_comm_init with its rank,

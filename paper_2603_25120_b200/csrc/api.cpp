@@ -502,15 +502,15 @@ static size_t balance_bound(uint32_t n, uint32_t m_max, uint32_t K, int device) 
            al256(slots * 2 * (2 * (size_t)n + 5 * (size_t)m_max + 16)) + al256((size_t)m_max * 4) * 2 + 4096;
 }
 
-static SearchLayout search_layout(uint32_t n, uint32_t P, uint64_t n_pairs, size_t bal_bytes, uint32_t n_bal,
-                                  int device) {
+static SearchLayout search_layout(uint32_t n_tot, uint32_t n_max, uint32_t P, uint32_t PD, uint64_t n_pairs,
+                                  size_t bal_bytes, uint32_t n_bal, int device) {
     SearchLayout L;
     size_t o = 0;
-    L.o_costs = o;   o += al256((size_t)P * 4 * n * 4);
-    L.o_results = o; o += al256((size_t)P * sizeof(dflop_cand_result));
-    L.o_assigns = o; o += al256((size_t)P * n * 4);
-    L.o_bcast = o;   o += al256(sizeof(dflop_cand_result) + (size_t)n * 4);
-    L.o_key = o;     o += 256;
+    L.o_costs = o;   o += al256((size_t)P * 4 * n_tot * 4);
+    L.o_results = o; o += al256((size_t)PD * sizeof(dflop_cand_result));
+    L.o_assigns = o; o += al256((size_t)P * n_tot * 4);
+    L.o_bcast = o;   o += al256(sizeof(dflop_cand_result) + (size_t)n_max * 4);
+    L.o_key = o;     o += al256(((size_t)PD + 1) * 8);
     L.o_stage_a = o; o += al256(stage_a_ws_bytes(n_pairs, device));
     L.o_top = o;     o += al256((size_t)P * sizeof(StageATop));
     L.o_feas = o;    o += 256;
@@ -531,12 +531,19 @@ static dflop_status nccl_status(ncclResult_t r, const char* what) {
 
 }  // namespace dflop
 
-extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_cost_model* cm,
-                                           const dflop_mem_model* mm, const uint32_t* tiles, const uint32_t* frames,
-                                           const uint32_t* text, uint32_t n, const dflop_search_params* sp,
-                                           dflop_comm* comm, void* ws, size_t* ws_bytes, dflop_plan_result* out,
-                                           uint32_t* assign, uint64_t* stage_a_out, uint64_t stage_a_cap,
-                                           dflop_stream_t stream) {
+namespace dflop {
+
+// a6 search over D batches (D = 1: dflop_search_plans; D > 1: Eq. (1) over the sample,
+// N2).  Batch b is samples [off[b], off[b+1]) of the concatenated features; its candidate
+// family uses Philox key (seed0, seed1 + b) (R33).  Stage A runs on the mean shapes of the
+// whole sample; Stage B balances every (top-P plan, batch); the plan minimises
+// (sum_b T_B(b), Stage-A rank) and every batch's winner is materialised for it.
+static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model* cm, const dflop_mem_model* mm,
+                                const uint32_t* tiles, const uint32_t* frames, const uint32_t* text,
+                                const uint32_t* off, uint32_t D, const dflop_search_params* sp, dflop_comm* comm,
+                                void* ws, size_t* ws_bytes, dflop_plan_result* out, dflop_cand_result* batch_out,
+                                uint64_t* plan_objective, uint32_t* assign, uint64_t* stage_a_out,
+                                uint64_t stage_a_cap, cudaStream_t s) {
     g_err.clear();
     dflop_status st = validate_cost_model(cm);
     if (st != DFLOP_OK) return st;
@@ -546,13 +553,25 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
     if (sp->K == 0 || sp->K > (1u << 24)) return invalid("K=%u outside 1..2^24", sp->K);
     if (sp->G < 1 || sp->G > 16) return invalid("G=%u outside 1..16", sp->G);
     if (sp->R > 4096) return invalid("R=%u > 4096", sp->R);
-    if (n > 65535) {
-        set_error("n=%u > 65535", n);
+    if (D < 1 || D > 4096) return invalid("batches D=%u outside 1..4096", D);
+    if (!off) return invalid("batch offsets are NULL");
+    uint32_t n_max = 0;
+    for (uint32_t b = 0; b < D; ++b) {
+        if (off[b + 1] < off[b]) return invalid("batch offsets must be non-decreasing");
+        n_max = std::max(n_max, off[b + 1] - off[b]);
+    }
+    const uint32_t n_tot = off[D] - off[0];
+    if (n_max > 65535) {
+        set_error("a batch of n=%u > 65535 samples", n_max);
         return DFLOP_ERR_SHAPE;
     }
-    if (n > 0 && (!tiles || !frames || !text)) return invalid("feature pointers must be non-NULL");
+    if (n_tot > 0 && (!tiles || !frames || !text)) return invalid("feature pointers must be non-NULL");
+    if ((uint64_t)sp->seed[1] + D - 1 > 0xFFFFFFFFull) return invalid("seed[1] + D - 1 overflows 32 bits");
+    tiles += off[0];
+    frames += off[0];
+    text += off[0];
     const int dev = current_device();
-    const uint32_t gbs = sp->gbs ? sp->gbs : n;
+    const uint32_t gbs = sp->gbs ? sp->gbs : n_max;
     const bool alg1 = sp->mode == DFLOP_SEARCH_ALG1;
     uint32_t P = 1, m_max = 0;
     const ConfigTable* tab = nullptr;
@@ -575,20 +594,21 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
         m_max = sp->fixed_plan.n_mb * sp->fixed_plan.l_dp;
     }
     // balance workspace: exact for a fixed plan, bounded for Algorithm 1 (plans unknown yet)
-    const int G_ = comm ? comm->world : 1, g_ = comm ? comm->rank : 0;
-    uint32_t sb, se;
-    shard(sp->K, g_, G_, &sb, &se);
+    const int G = comm ? comm->world : 1, g = comm ? comm->rank : 0;
+    uint32_t cb, cend;
+    shard(sp->K, g, G, &cb, &cend);
     size_t bal_bytes = 0;
     if (alg1) {
-        bal_bytes = balance_bound(n, std::max(1u, m_max), std::max(1u, se - sb), dev);
-    } else if (se > sb) {
+        bal_bytes = balance_bound(n_max, std::max(1u, m_max), std::max(1u, cend - cb), dev);
+    } else if (cend > cb) {
         BalancePlan bp0;
-        if ((st = plan_balance(n, &sp->fixed_plan, DFLOP_MODE_HEURISTIC, sp->R, sp->G, se - sb, &bp0)) != DFLOP_OK)
+        if ((st = plan_balance(n_max, &sp->fixed_plan, DFLOP_MODE_HEURISTIC, sp->R, sp->G, cend - cb, &bp0)) != DFLOP_OK)
             return st;
         bal_bytes = bp0.cfg.total;
     }
-    const SearchLayout L =
-        search_layout(n, P, tab ? tab->n_pairs : 0, bal_bytes, alg1 ? std::min(P, stage_b_streams()) : 1u, dev);
+    const uint32_t PD = P * D;
+    const SearchLayout L = search_layout(n_tot, n_max, P, PD, tab ? tab->n_pairs : 0, bal_bytes,
+                                         std::min(PD, stage_b_streams()), dev);
     if (!ws) {
         *ws_bytes = L.total;
         return DFLOP_OK;
@@ -599,18 +619,16 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
     }
     if ((uintptr_t)ws % 256) return invalid("workspace must be 256-byte aligned");
     if (!out) return invalid("out is NULL");
-    cudaStream_t s = (cudaStream_t)stream;
     char* w = reinterpret_cast<char*>(ws);
-    uint32_t* costs = reinterpret_cast<uint32_t*>(w + L.o_costs);
-    dflop_cand_result* results = reinterpret_cast<dflop_cand_result*>(w + L.o_results);
-    uint32_t* assigns = reinterpret_cast<uint32_t*>(w + L.o_assigns);
+    uint32_t* costs = reinterpret_cast<uint32_t*>(w + L.o_costs);              // [P][4][n_tot]
+    dflop_cand_result* results = reinterpret_cast<dflop_cand_result*>(w + L.o_results);  // [P][D]
+    uint32_t* assigns = reinterpret_cast<uint32_t*>(w + L.o_assigns);          // [P][n_tot]
     char* bcast = w + L.o_bcast;
-    uint64_t* d_key = reinterpret_cast<uint64_t*>(w + L.o_key);
+    uint64_t* d_key = reinterpret_cast<uint64_t*>(w + L.o_key);                // [P*D] keys + 2 u32
     StageATop* d_top = reinterpret_cast<StageATop*>(w + L.o_top);
     unsigned long long* d_feas = reinterpret_cast<unsigned long long*>(w + L.o_feas);
     uint32_t* d_status = reinterpret_cast<uint32_t*>(w + L.o_status);
     void* bal_ws = w + L.o_bal;
-    const int G = comm ? comm->world : 1, g = comm ? comm->rank : 0;
 
     dflop_plan_result res;
     memset(&res, 0, sizeof res);
@@ -624,8 +642,8 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
         res.n_configs = nc;
         res.n_pairs = tab->n_pairs;
         uint64_t* sa_out = (stage_a_out && stage_a_cap >= tab->n_pairs) ? stage_a_out : nullptr;
-        if ((st = stage_a_launch(cm, mm, tab->d_cfgs, tab->d_pair_start, nc, tab->n_pairs, gbs, tiles, frames, text, n,
-                                 P, w + L.o_stage_a, sa_out, d_top, d_feas, s)) != DFLOP_OK)
+        if ((st = stage_a_launch(cm, mm, tab->d_cfgs, tab->d_pair_start, nc, tab->n_pairs, gbs, tiles, frames, text,
+                                 n_tot, P, w + L.o_stage_a, sa_out, d_top, d_feas, s)) != DFLOP_OK)
             return st;
         std::vector<StageATop> top(P);
         unsigned long long feas = 0;
@@ -654,16 +672,22 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
         plans.push_back(sp->fixed_plan);
         plan_TA.push_back(0);
     }
-    // ---- Stage B: a1 for every plan in one launch, then a2..a5 per plan on this rank's shard
+    // ---- Stage B: per batch a1 for every plan in one launch, then a2..a5 per (plan, batch) on
+    // this rank's shard; (plan, batch) pairs round-robin over the Stage-B streams
     const uint32_t np = (uint32_t)plans.size();
     std::vector<PredictConsts> kc(np);
     for (uint32_t p = 0; p < np; ++p) kc[p] = predict_consts(cm, &plans[p]);
-    ce = predict_launch(cm, kc.data(), np, tiles, frames, text, n, nullptr, costs, (size_t)4 * n, d_status, s);
-    if (ce != cudaSuccess) return cuda_status(ce, "predict launch");
-    uint32_t cb, cend;
-    shard(sp->K, g, G, &cb, &cend);
-    // fork: plan p runs on stream p % ns with balance workspace p % ns; joined below
-    const uint32_t ns = std::min<uint32_t>(L.n_bal, np);
+    const size_t pstride = (size_t)4 * n_tot;  // one plan's [4][n_tot] costs
+    for (uint32_t b = 0; b < D; ++b) {
+        const uint32_t o = off[b] - off[0], nb = off[b + 1] - off[b];
+        if (nb == 0) continue;
+        // the batch's [4][nb] rows inside each plan's [4][n_tot] block: row r at r*n_tot + o
+        ce = predict_launch_rows(cm, kc.data(), np, tiles + o, frames + o, text + o, nb, costs + o, n_tot, pstride,
+                                 d_status, s);
+        if (ce != cudaSuccess) return cuda_status(ce, "predict launch");
+    }
+    const uint32_t n_pairs_b = np * D;
+    const uint32_t ns = std::min<uint32_t>(L.n_bal, n_pairs_b);
     std::vector<cudaStream_t> ss(ns, s);
     struct Events {
         std::vector<cudaEvent_t> ev;
@@ -687,117 +711,156 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
         }
     }
     for (uint32_t p = 0; p < np; ++p) {
-        BalancePlan bpn;
-        cudaStream_t sp_s = ss[p % ns];
-        if (cb >= cend) {
-            // empty shard on this rank: mark the plan's result as "no candidate"
-            ce = cudaMemsetAsync(&results[p], 0xFF, sizeof(dflop_cand_result), sp_s);
-            if (ce != cudaSuccess) return cuda_status(ce, "memset");
-            continue;
+        for (uint32_t b = 0; b < D; ++b) {
+            const uint32_t q = p * D + b, o = off[b] - off[0], nb = off[b + 1] - off[b];
+            cudaStream_t sq = ss[q % ns];
+            if (cb >= cend) {
+                // empty shard on this rank: mark the (plan, batch) result as "no candidate"
+                ce = cudaMemsetAsync(&results[q], 0xFF, sizeof(dflop_cand_result), sq);
+                if (ce != cudaSuccess) return cuda_status(ce, "memset");
+                continue;
+            }
+            BalancePlan bpn;
+            if ((st = plan_balance(nb, &plans[p], DFLOP_MODE_HEURISTIC, sp->R, sp->G, cend - cb, &bpn)) != DFLOP_OK)
+                return st;
+            if (bpn.cfg.total > L.bal_bytes) {
+                set_error("internal: balance workspace %zu > bound %zu", bpn.cfg.total, L.bal_bytes);
+                return DFLOP_ERR_UNSUPPORTED;
+            }
+            BalanceArgs a{};
+            a.cost_ticks = costs + (size_t)p * pstride + o;
+            a.cost_stride = n_tot;
+            a.sh = bpn.sh;
+            a.K = sp->K;
+            a.c_begin = cb;
+            a.c_end = cend;
+            a.seed0 = sp->seed[0];
+            a.seed1 = sp->seed[1] + b;
+            a.id_base = p * sp->K;
+            a.ws = reinterpret_cast<char*>(bal_ws) + (size_t)(q % ns) * L.bal_stride;
+            a.best = &results[q];
+            a.assign = assigns + (size_t)p * n_tot + o;
+            if ((st = balance_launch(a, bpn.cfg, bpn.prog, sq)) != DFLOP_OK) return st;
         }
-        if ((st = plan_balance(n, &plans[p], DFLOP_MODE_HEURISTIC, sp->R, sp->G, cend - cb, &bpn)) != DFLOP_OK)
-            return st;
-        if (bpn.cfg.total > L.bal_bytes) {
-            set_error("internal: balance workspace %zu > bound %zu", bpn.cfg.total, L.bal_bytes);
-            return DFLOP_ERR_UNSUPPORTED;
-        }
-        BalanceArgs a{};
-        a.cost_ticks = costs + (size_t)p * 4 * n;
-        a.sh = bpn.sh;
-        a.K = sp->K;
-        a.c_begin = cb;
-        a.c_end = cend;
-        a.seed0 = sp->seed[0];
-        a.seed1 = sp->seed[1];
-        a.id_base = p * sp->K;
-        a.ws = reinterpret_cast<char*>(bal_ws) + (size_t)(p % ns) * L.bal_stride;
-        a.best = &results[p];
-        a.assign = assigns + (size_t)p * n;
-        if ((st = balance_launch(a, bpn.cfg, bpn.prog, sp_s)) != DFLOP_OK) return st;
     }
     for (uint32_t k = 1; k < ns; ++k) {  // join
         cudaEvent_t j = evs.make();
         if (!j || cudaEventRecord(j, ss[k]) != cudaSuccess) return cuda_status(cudaGetLastError(), "join event");
         if ((ce = cudaStreamWaitEvent(s, j, 0)) != cudaSuccess) return cuda_status(ce, "join wait");
     }
-    // ---- local argmin over plans, then the NCCL min all-reduce of the packed key
-    std::vector<dflop_cand_result> hres(np);
-    ce = cudaMemcpyAsync(hres.data(), results, np * sizeof(dflop_cand_result), cudaMemcpyDeviceToHost, s);
+    // ---- per (plan, batch) local keys, one NCCL min all-reduce of the [P*D] key array
+    std::vector<dflop_cand_result> hres(n_pairs_b);
+    ce = cudaMemcpyAsync(hres.data(), results, n_pairs_b * sizeof(dflop_cand_result), cudaMemcpyDeviceToHost, s);
     uint32_t hstatus = 0;
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(&hstatus, d_status, 4, cudaMemcpyDeviceToHost, s);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) return cuda_status(ce, "stage B readback");
-    uint64_t local = ~0ull;
-    uint32_t local_p = 0;
-    for (uint32_t p = 0; p < np; ++p) {
-        if (hres[p].key < local) {
-            local = hres[p].key;
-            local_p = p;
-        }
-        if (hres[p].key != ~0ull) hstatus |= hres[p].status;
+    std::vector<uint64_t> keys(n_pairs_b + 1);
+    for (uint32_t q = 0; q < n_pairs_b; ++q) {
+        keys[q] = hres[q].key;
+        if (hres[q].key != ~0ull) hstatus |= hres[q].status;
     }
-    uint64_t global = local;
     uint32_t gstatus = hstatus;
     if (comm && G > 1) {
-        // one 8-byte min for the packed (T, id) key; the status bits travel as a max over
-        // per-bit flags so that any rank's bit survives
-        static thread_local uint32_t bits[2];
-        bits[0] = hstatus & 1u;
-        bits[1] = (hstatus >> 1) & 1u;
-        uint32_t* d_bits = reinterpret_cast<uint32_t*>(d_key + 1);
-        ce = cudaMemcpyAsync(d_key, &local, 8, cudaMemcpyHostToDevice, s);
-        if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_bits, bits, 8, cudaMemcpyHostToDevice, s);
+        // the status bits travel as a max over per-bit flags so that any rank's bit survives
+        uint32_t bits[2] = {hstatus & 1u, (hstatus >> 1) & 1u};
+        memcpy(&keys[n_pairs_b], bits, 8);
+        ce = cudaMemcpyAsync(d_key, keys.data(), (n_pairs_b + 1) * 8, cudaMemcpyHostToDevice, s);
         if (ce != cudaSuccess) return cuda_status(ce, "key upload");
+        uint32_t* d_bits = reinterpret_cast<uint32_t*>(d_key + n_pairs_b);
         ncclResult_t r = ncclGroupStart();
-        if (r == ncclSuccess) r = ncclAllReduce(d_key, d_key, 1, ncclUint64, ncclMin, comm->comm, s);
+        if (r == ncclSuccess) r = ncclAllReduce(d_key, d_key, n_pairs_b, ncclUint64, ncclMin, comm->comm, s);
         if (r == ncclSuccess) r = ncclAllReduce(d_bits, d_bits, 2, ncclUint32, ncclMax, comm->comm, s);
         if (r == ncclSuccess) r = ncclGroupEnd();
-        if ((st = nccl_status(r, "ncclAllReduce(min key)")) != DFLOP_OK) return st;
-        ce = cudaMemcpyAsync(&global, d_key, 8, cudaMemcpyDeviceToHost, s);
-        if (ce == cudaSuccess) ce = cudaMemcpyAsync(bits, d_bits, 8, cudaMemcpyDeviceToHost, s);
+        if ((st = nccl_status(r, "ncclAllReduce(min keys)")) != DFLOP_OK) return st;
+        ce = cudaMemcpyAsync(keys.data(), d_key, (n_pairs_b + 1) * 8, cudaMemcpyDeviceToHost, s);
         if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
         if (ce != cudaSuccess) return cuda_status(ce, "key readback");
+        memcpy(bits, &keys[n_pairs_b], 8);
         gstatus = bits[0] | (bits[1] << 1);
     }
-    if (global == ~0ull) {
+    // ---- the plan: argmin over p of (sum_b T_B(b, p), p); for D = 1 the packed key order
+    // (T_B, p, c) -- the same choice
+    uint32_t win_p = 0xFFFFFFFFu;
+    uint64_t best_obj = ~0ull;
+    for (uint32_t p = 0; p < np; ++p) {
+        uint64_t obj = 0;
+        bool ok = true;
+        for (uint32_t b = 0; b < D; ++b) {
+            const uint64_t k = keys[p * D + b];
+            if (off[b + 1] == off[b]) continue;  // an empty batch contributes 0
+            if (k == ~0ull) {
+                ok = false;
+                break;
+            }
+            obj += k >> 24;
+        }
+        if (plan_objective) plan_objective[p] = ok ? obj : ~0ull;
+        if (ok && obj < best_obj) {
+            best_obj = obj;
+            win_p = p;
+        }
+    }
+    if (win_p == 0xFFFFFFFFu) {
         set_error("no candidate evaluated");
         return DFLOP_ERR_UNSUPPORTED;
     }
-    const uint32_t id = (uint32_t)(global & 0xFFFFFFull);
-    const uint32_t win_p = id / sp->K, win_c = id % sp->K;
-    const int owner = owner_of(sp->K, win_c, G);
-    // winner's record + assignment: owner packs, NCCL broadcasts (G > 1)
-    if (g == owner) {
-        ce = cudaMemcpyAsync(bcast, &results[win_p], sizeof(dflop_cand_result), cudaMemcpyDeviceToDevice, s);
-        if (ce == cudaSuccess && n > 0)
-            ce = cudaMemcpyAsync(bcast + sizeof(dflop_cand_result), assigns + (size_t)win_p * n, (size_t)n * 4,
-                                 cudaMemcpyDeviceToDevice, s);
-        if (ce != cudaSuccess) return cuda_status(ce, "winner pack");
+    // ---- every batch's winner of plan win_p: the owner packs, NCCL broadcasts (G > 1)
+    dflop_cand_result first{};
+    uint32_t first_c = 0;
+    int first_owner = 0;
+    for (uint32_t b = 0; b < D; ++b) {
+        const uint32_t q = win_p * D + b, o = off[b] - off[0], nb = off[b + 1] - off[b];
+        dflop_cand_result win;
+        memset(&win, 0, sizeof win);
+        uint32_t win_c = 0;
+        int owner = 0;
+        if (nb > 0 || D == 1) {
+            const uint64_t key = keys[q];
+            const uint32_t id = (uint32_t)(key & 0xFFFFFFull);
+            win_c = id - win_p * sp->K;
+            owner = owner_of(sp->K, win_c, G);
+            if (g == owner) {
+                ce = cudaMemcpyAsync(bcast, &results[q], sizeof(dflop_cand_result), cudaMemcpyDeviceToDevice, s);
+                if (ce == cudaSuccess && nb > 0)
+                    ce = cudaMemcpyAsync(bcast + sizeof(dflop_cand_result), assigns + (size_t)win_p * n_tot + o,
+                                         (size_t)nb * 4, cudaMemcpyDeviceToDevice, s);
+                if (ce != cudaSuccess) return cuda_status(ce, "winner pack");
+            }
+            if (comm && G > 1) {
+                ncclResult_t r = ncclBroadcast(bcast, bcast, sizeof(dflop_cand_result) + (size_t)nb * 4, ncclUint8,
+                                               owner, comm->comm, s);
+                if ((st = nccl_status(r, "ncclBroadcast(winner)")) != DFLOP_OK) return st;
+            }
+            if (assign && nb > 0) {
+                ce = cudaMemcpyAsync(assign + o, bcast + sizeof(dflop_cand_result), (size_t)nb * 4,
+                                     cudaMemcpyDeviceToDevice, s);
+                if (ce != cudaSuccess) return cuda_status(ce, "assign copy");
+            }
+            ce = cudaMemcpyAsync(&win, bcast, sizeof win, cudaMemcpyDeviceToHost, s);
+            if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+            if (ce != cudaSuccess) return cuda_status(ce, "winner readback");
+        }
+        win.cand = win_c;
+        if (batch_out) batch_out[b] = win;
+        if (b == 0) {
+            first = win;
+            first_c = win_c;
+            first_owner = owner;
+        }
+        gstatus |= win.status;
     }
-    if (comm && G > 1) {
-        ncclResult_t r = ncclBroadcast(bcast, bcast, sizeof(dflop_cand_result) + (size_t)n * 4, ncclUint8, owner,
-                                       comm->comm, s);
-        if ((st = nccl_status(r, "ncclBroadcast(winner)")) != DFLOP_OK) return st;
-    }
-    dflop_cand_result win;
-    if (assign && n > 0) {
-        ce = cudaMemcpyAsync(assign, bcast + sizeof(dflop_cand_result), (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
-        if (ce != cudaSuccess) return cuda_status(ce, "assign copy");
-    }
-    ce = cudaMemcpyAsync(&win, bcast, sizeof win, cudaMemcpyDeviceToHost, s);
-    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
-    if (ce != cudaSuccess) return cuda_status(ce, "winner readback");
-    res.status_bits = gstatus | win.status;
+    res.status_bits = gstatus;
     res.plan = plans[win_p];
     res.m = plans[win_p].n_mb * plans[win_p].l_dp;
-    res.cand = win_c;
+    res.cand = first_c;
     res.stage_a_rank = alg1 ? win_p : 0;
-    res.owner_rank = (uint32_t)owner;
-    res.makespan = win.makespan;
-    res.cmax = win.cmax;
+    res.owner_rank = (uint32_t)first_owner;
+    res.makespan = D == 1 ? first.makespan : best_obj;
+    res.cmax = first.cmax;
     res.stage_a_makespan = plan_TA[win_p];
     if (!alg1) res.alg1_plan = plans[0];
-    res.n_candidates = (uint64_t)np * sp->K;
+    res.n_candidates = (uint64_t)np * D * sp->K;
     *out = res;
     if (res.status_bits & DFLOP_DEV_COST_OVERFLOW) {
         set_error("a predicted stage cost rounded to >= 2^32 ticks; raise tick_ns");
@@ -808,4 +871,29 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
         return DFLOP_ERR_OVERFLOW;
     }
     return DFLOP_OK;
+}
+
+}  // namespace dflop
+
+extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_cost_model* cm,
+                                           const dflop_mem_model* mm, const uint32_t* tiles, const uint32_t* frames,
+                                           const uint32_t* text, uint32_t n, const dflop_search_params* sp,
+                                           dflop_comm* comm, void* ws, size_t* ws_bytes, dflop_plan_result* out,
+                                           uint32_t* assign, uint64_t* stage_a_out, uint64_t stage_a_cap,
+                                           dflop_stream_t stream) {
+    const uint32_t off[2] = {0, n};
+    return search_impl(cl, cm, mm, tiles, frames, text, off, 1, sp, comm, ws, ws_bytes, out, nullptr, nullptr, assign,
+                       stage_a_out, stage_a_cap, (cudaStream_t)stream);
+}
+
+extern "C" dflop_status dflop_search_plans_batches(const dflop_cluster* cl, const dflop_cost_model* cm,
+                                                   const dflop_mem_model* mm, const uint32_t* tiles,
+                                                   const uint32_t* frames, const uint32_t* text,
+                                                   const uint32_t* batch_offsets, uint32_t n_batches,
+                                                   const dflop_search_params* sp, dflop_comm* comm, void* ws,
+                                                   size_t* ws_bytes, dflop_plan_result* out,
+                                                   dflop_cand_result* batch_results, uint64_t* plan_objective,
+                                                   uint32_t* assign, dflop_stream_t stream) {
+    return search_impl(cl, cm, mm, tiles, frames, text, batch_offsets, n_batches, sp, comm, ws, ws_bytes, out,
+                       batch_results, plan_objective, assign, nullptr, 0, (cudaStream_t)stream);
 }

@@ -36,11 +36,12 @@ __global__ void k_init(BalanceHeader* hdr, u64* slot_key, uint32_t n_slots) {
     for (uint32_t s = t; s < n_slots; s += gridDim.x * blockDim.x) slot_key[s] = ~0ull;
 }
 
-__global__ void k_prep_keys(const uint32_t* __restrict__ cost, uint32_t n, BalanceHeader* hdr, u64* keys) {
+// cost rows: ef, eb, lf, lb at cost + r * rs (rs >= n: the row stride)
+__global__ void k_prep_keys(const uint32_t* __restrict__ cost, uint32_t n, size_t rs, BalanceHeader* hdr, u64* keys) {
     u64 se = 0, sl = 0, mk = 0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const u64 e = (u64)cost[i] + cost[(size_t)n + i];
-        const u64 l = (u64)cost[2 * (size_t)n + i] + cost[3 * (size_t)n + i];
+        const u64 e = (u64)cost[i] + cost[rs + i];
+        const u64 l = (u64)cost[2 * rs + i] + cost[3 * rs + i];
         const u64 k = e > l ? e : l;
         keys[i] = k;
         se += e;
@@ -90,7 +91,7 @@ __global__ void k_rank_sort(const u64* __restrict__ keys, uint32_t n, uint32_t* 
 //   2^(32 - s), s = bits of m - 1:
 //   a probe's winner has W <= min_j W_j + max(e, l) <= (sum_e + sum_l)/m + max key, every
 //   probe adds at most one more max key, and refinement never raises the maximum (O6).
-__global__ void k_build_items(const uint32_t* __restrict__ cost, uint32_t n, uint32_t m, uint32_t allow_pack,
+__global__ void k_build_items(const uint32_t* __restrict__ cost, uint32_t n, size_t rs, uint32_t m, uint32_t allow_pack,
                               BalanceHeader* hdr, const uint32_t* __restrict__ order, ItemRec<uint32_t>* it32,
                               ItemRec<u64>* it64) {
     const bool fits = hdr->sum_e < 0xFFFFFFFFull && hdr->sum_l < 0xFFFFFFFFull;
@@ -104,8 +105,7 @@ __global__ void k_build_items(const uint32_t* __restrict__ cost, uint32_t n, uin
     }
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const uint32_t i = order[t];
-        const uint32_t ef = cost[i], eb = cost[(size_t)n + i], lf = cost[2 * (size_t)n + i],
-                       lb = cost[3 * (size_t)n + i];
+        const uint32_t ef = cost[i], eb = cost[rs + i], lf = cost[2 * rs + i], lb = cost[3 * rs + i];
         if (fits)
             // packed variant: e and l pre-shifted into the key position (E << s | j sums)
             it32[t] = packed ? ItemRec<uint32_t>{(ef + eb) << sh, (lf + lb) << sh, ef, lf}
@@ -408,11 +408,12 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
                                                                                           cfg.n_slots);
     if (n > 0) {
         const uint32_t gb = std::min<uint32_t>((n + 255) / 256, 592);
-        k_prep_keys<<<gb, 256, 0, s>>>(a.cost_ticks, n, hdr, keys);
+        const size_t rs = a.cost_stride ? a.cost_stride : n;
+        k_prep_keys<<<gb, 256, 0, s>>>(a.cost_ticks, n, rs, hdr, keys);
         k_rank_sort<<<(n + 255) / 256, 256, 0, s>>>(keys, n, order, item_pos);
-        k_build_items<<<gb, 256, 0, s>>>(a.cost_ticks, n, a.sh.m, allow_pack, hdr, order, it32, it64);
+        k_build_items<<<gb, 256, 0, s>>>(a.cost_ticks, n, rs, a.sh.m, allow_pack, hdr, order, it32, it64);
     } else {
-        k_build_items<<<1, 32, 0, s>>>(a.cost_ticks, 0, a.sh.m, allow_pack, hdr, order, it32, it64);
+        k_build_items<<<1, 32, 0, s>>>(a.cost_ticks, 0, 0, a.sh.m, allow_pack, hdr, order, it32, it64);
     }
     CandParams p{};
     p.pos_item = order;

@@ -42,6 +42,11 @@ cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* const
                            const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
                            float* cost_f32, uint32_t* cost_ticks, size_t plan_stride, uint32_t* dev_status,
                            cudaStream_t s);
+// ticks only, rows `row_stride` apart inside each plan's block of plan_stride entries
+cudaError_t predict_launch_rows(const dflop_cost_model* m, const PredictConsts* consts, uint32_t n_plans,
+                                const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
+                                uint32_t* cost_ticks, size_t row_stride, size_t plan_stride, uint32_t* dev_status,
+                                cudaStream_t s);
 
 // ---------------------------------------------------------------- 1F1B slot program
 struct SlotProgram {
@@ -85,7 +90,8 @@ struct BalanceConfig {
 BalanceConfig balance_config(const BalanceShape& sh, int device);
 // Launches the whole a2..a5 sequence for one plan on `stream`.
 struct BalanceArgs {
-    const uint32_t* cost_ticks;
+    const uint32_t* cost_ticks;  // rows ef, eb, lf, lb of n entries, cost_stride apart (0 = n)
+    size_t cost_stride;
     BalanceShape sh;
     uint32_t K, c_begin, c_end, seed0, seed1, id_base;
     void* ws;

@@ -75,7 +75,7 @@ template <bool VEC>
 __global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaunch L, const uint32_t* __restrict__ tiles,
                                                  const uint32_t* __restrict__ frames, const uint32_t* __restrict__ text,
                                                  uint32_t n, float* cost_f32, uint32_t* cost_ticks, size_t plan_stride,
-                                                 uint32_t* dev_status) {
+                                                 size_t rs, uint32_t* dev_status) {
     __shared__ PredictGrids g;
     __shared__ PredictPlan pp;
     for (uint32_t w = threadIdx.x; w < sizeof(PredictGrids) / 4; w += blockDim.x)
@@ -131,11 +131,11 @@ __global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaun
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             if (VEC) {
-                if (f32) reinterpret_cast<float4*>(f32 + (size_t)r * n)[q] = make_float4(o[r][0], o[r][1], o[r][2], o[r][3]);
-                if (tk) reinterpret_cast<uint4*>(tk + (size_t)r * n)[q] = make_uint4(t4[r][0], t4[r][1], t4[r][2], t4[r][3]);
+                if (f32) reinterpret_cast<float4*>(f32 + (size_t)r * rs)[q] = make_float4(o[r][0], o[r][1], o[r][2], o[r][3]);
+                if (tk) reinterpret_cast<uint4*>(tk + (size_t)r * rs)[q] = make_uint4(t4[r][0], t4[r][1], t4[r][2], t4[r][3]);
             } else {
-                if (f32) f32[(size_t)r * n + q] = o[r][0];
-                if (tk) tk[(size_t)r * n + q] = t4[r][0];
+                if (f32) f32[(size_t)r * rs + q] = o[r][0];
+                if (tk) tk[(size_t)r * rs + q] = t4[r][0];
             }
         }
     }
@@ -194,10 +194,10 @@ PredictConsts predict_consts(const dflop_cost_model* m, const dflop_plan* p) {
     return k;
 }
 
-cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* consts, uint32_t n_plans,
-                           const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
-                           float* cost_f32, uint32_t* cost_ticks, size_t plan_stride, uint32_t* dev_status,
-                           cudaStream_t s) {
+static cudaError_t predict_impl(const dflop_cost_model* m, const PredictConsts* consts, uint32_t n_plans,
+                                const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
+                                float* cost_f32, uint32_t* cost_ticks, size_t rs, size_t plan_stride,
+                                uint32_t* dev_status, cudaStream_t s) {
     if (n == 0 || n_plans == 0) return cudaSuccess;
     PredictGrids g;
     to_knots(m->thr_e, g.e);
@@ -209,7 +209,7 @@ cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* const
     g.pad[0] = g.pad[1] = g.pad[2] = 0;
     const bool vec = (n % 4 == 0) && ((uintptr_t)tiles % 16 == 0) && ((uintptr_t)frames % 16 == 0) &&
                      ((uintptr_t)text % 16 == 0) && (!cost_f32 || (uintptr_t)cost_f32 % 16 == 0) &&
-                     (!cost_ticks || (uintptr_t)cost_ticks % 16 == 0) && (plan_stride % 4 == 0);
+                     (!cost_ticks || (uintptr_t)cost_ticks % 16 == 0) && (plan_stride % 4 == 0) && (rs % 4 == 0);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -228,12 +228,27 @@ cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* const
         float* f = cost_f32 ? cost_f32 + (size_t)p0 * plan_stride : nullptr;
         uint32_t* t = cost_ticks ? cost_ticks + (size_t)p0 * plan_stride : nullptr;
         if (vec)
-            k_predict<true><<<grid, 256, 0, s>>>(g, L, tiles, frames, text, n, f, t, plan_stride, dev_status);
+            k_predict<true><<<grid, 256, 0, s>>>(g, L, tiles, frames, text, n, f, t, plan_stride, rs, dev_status);
         else
-            k_predict<false><<<grid, 256, 0, s>>>(g, L, tiles, frames, text, n, f, t, plan_stride, dev_status);
+            k_predict<false><<<grid, 256, 0, s>>>(g, L, tiles, frames, text, n, f, t, plan_stride, rs, dev_status);
         count_launches(1);
     }
     return cudaGetLastError();
+}
+
+cudaError_t predict_launch(const dflop_cost_model* m, const PredictConsts* consts, uint32_t n_plans,
+                           const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
+                           float* cost_f32, uint32_t* cost_ticks, size_t plan_stride, uint32_t* dev_status,
+                           cudaStream_t s) {
+    return predict_impl(m, consts, n_plans, tiles, frames, text, n, cost_f32, cost_ticks, n, plan_stride, dev_status, s);
+}
+
+cudaError_t predict_launch_rows(const dflop_cost_model* m, const PredictConsts* consts, uint32_t n_plans,
+                                const uint32_t* tiles, const uint32_t* frames, const uint32_t* text, uint32_t n,
+                                uint32_t* cost_ticks, size_t row_stride, size_t plan_stride, uint32_t* dev_status,
+                                cudaStream_t s) {
+    return predict_impl(m, consts, n_plans, tiles, frames, text, n, nullptr, cost_ticks, row_stride, plan_stride,
+                        dev_status, s);
 }
 
 }  // namespace dflop

@@ -11,6 +11,8 @@ import ctypes as C
 import os
 from typing import Dict, Optional, Sequence
 
+import numpy as np
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DFLOP_LIB") or os.path.join(HERE, "libdflop.so")
 
@@ -24,7 +26,7 @@ STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE", 3: "OVERFLOW", 4: "INFEASI
 EXPORTS = ["dflop_abi_version", "dflop_last_error", "dflop_release_caches", "dflop_predict_costs",
            "dflop_balance_microbatches", "dflop_simulate_1f1b", "dflop_index_groups", "dflop_search_plans",
            "dflop_get_unique_id", "dflop_comm_init", "dflop_comm_destroy", "dflop_profile_enable",
-           "dflop_profile_read"]
+           "dflop_profile_read", "dflop_search_plans_batches"]
 
 
 class DflopError(RuntimeError):
@@ -377,6 +379,61 @@ def search_plans(model: Dict, tiles, frames, text, K: int, R: int, G: int, seed:
     r = {f: getattr(out, f) for f, _ in PlanResult._fields_ if f not in ("plan", "alg1_plan", "reserved")}
     r["plan"] = out.plan.as_dict()
     r["alg1_plan"] = out.alg1_plan.as_dict()
+    r["assign"] = assign[:n] if assign is not None else None
+    return r
+
+
+def search_plans_batches(model: Dict, tiles, frames, text, batch_offsets: Sequence[int], K: int, R: int, G: int,
+                         seed: Sequence[int], plan: Optional[Dict] = None, cluster: Optional[Dict] = None,
+                         mem: Optional[Dict] = None, gbs: int = 0, top_p: int = 1, comm=None,
+                         want_assign: bool = True, ws: Optional[Workspace] = None, stream=None) -> Dict:
+    """N2, Eq. (1) over a sample of D batches (synchronous): batch b = samples
+    [batch_offsets[b], batch_offsets[b+1]) of the concatenated features; its family uses
+    Philox key (seed[0], seed[1] + b).  Returns the dflop_plan_result fields (makespan =
+    sum_b T_B(b) of theta*), 'batches' (per-batch winners), 'plan_objective' and 'assign'."""
+    import torch
+    offs = np.ascontiguousarray(np.asarray(batch_offsets, np.uint32))
+    D = len(offs) - 1
+    n = int(offs[-1] - offs[0])
+    dev = tiles.device
+    sp = SearchParams()
+    sp.struct_size = C.sizeof(SearchParams)
+    sp.mode = SEARCH_FIXED if plan is not None else SEARCH_ALG1
+    if plan is not None:
+        sp.fixed_plan = plan_struct(plan)
+    sp.gbs, sp.top_p, sp.K, sp.R, sp.G = gbs, top_p, K, R, G
+    sp.seed[0], sp.seed[1] = int(seed[0]) & 0xFFFFFFFF, int(seed[1]) & 0xFFFFFFFF
+    ms = cost_model_struct(model)
+    cl = Cluster()
+    mm = MemModel()
+    if cluster is not None:
+        cl.struct_size = C.sizeof(Cluster)
+        cl.n_gpus, cl.gpus_per_node = cluster["n_gpus"], cluster["gpus_per_node"]
+    if mem is not None:
+        mm = mem_model_struct(mem)
+    cptr = C.c_void_p(comm.handle) if comm is not None else None
+    L = lib()
+    op = offs.ctypes.data_as(C.c_void_p)
+    need = C.c_size_t(0)
+    out = PlanResult()
+    _check(L.dflop_search_plans_batches(C.byref(cl), C.byref(ms), C.byref(mm), _ptr(tiles), _ptr(frames), _ptr(text),
+                                        op, D, C.byref(sp), cptr, None, C.byref(need), C.byref(out), None, None,
+                                        None, None))
+    wsb = (ws or _default_ws).get(need.value, dev)
+    assign = torch.empty(max(n, 1), dtype=torch.int32, device=dev) if want_assign else None
+    have = C.c_size_t(wsb.numel())
+    bres = (CandResult * D)()
+    P = top_p if plan is None else 1
+    pobj = np.zeros(P, np.uint64)
+    _check(L.dflop_search_plans_batches(C.byref(cl), C.byref(ms), C.byref(mm), _ptr(_u32(tiles)), _ptr(_u32(frames)),
+                                        _ptr(_u32(text)), op, D, C.byref(sp), cptr, _ptr(wsb), C.byref(have),
+                                        C.byref(out), bres, pobj.ctypes.data_as(C.c_void_p), _ptr(assign),
+                                        _stream(stream)))
+    r = {f: getattr(out, f) for f, _ in PlanResult._fields_ if f not in ("plan", "alg1_plan", "reserved")}
+    r["plan"] = out.plan.as_dict()
+    r["alg1_plan"] = out.alg1_plan.as_dict()
+    r["batches"] = [dict(key=b.key, makespan=b.makespan, cmax=b.cmax, cand=b.cand, status=b.status) for b in bres]
+    r["plan_objective"] = pobj
     r["assign"] = assign[:n] if assign is not None else None
     return r
 

@@ -25,14 +25,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("k", [2, 3, 5])
-def test_sharded_search_equals_single_gpu(k):
+@pytest.mark.parametrize("k, batches", [(2, 0), (3, 0), (5, 0), (2, 3)])
+def test_sharded_search_equals_single_gpu(k, batches):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(min(n, 2)),
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "dist_check.py"),
-           "--config", str(k), "--K", "4096"]
+           "--config", str(k), "--K", "4096", "--batches", str(batches)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]

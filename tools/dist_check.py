@@ -24,21 +24,33 @@ from paper_2603_25120_b200 import sharding, synth
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--K", type=int, default=8192)
+ap.add_argument("--batches", type=int, default=0, help="N2: Eq. (1) over this many batches (0 = one batch)")
 a = ap.parse_args()
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 p = synth.presets()[a.config]
-t, f, x = (torch.from_numpy(v.astype(np.uint32).view(np.int32)).cuda() for v in p.features(0))
 comm = D.Comm(rank, world, local)
-res = D.search_plans(p.model, t, f, x, K=a.K, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan, comm=comm)
+if a.batches:
+    feats = [p.features(b) for b in range(a.batches)]
+    offs = np.concatenate([[0], np.cumsum([len(fb[0]) for fb in feats])])
+    t, f, x = (torch.from_numpy(np.concatenate([fb[i] for fb in feats]).astype(np.uint32).view(np.int32)).cuda()
+               for i in range(3))
+    run = lambda cm: D.search_plans_batches(p.model, t, f, x, offs, K=a.K, R=p.R, G=p.G, seed=p.seed(0),
+                                            plan=p.plan, comm=cm)
+else:
+    t, f, x = (torch.from_numpy(v.astype(np.uint32).view(np.int32)).cuda() for v in p.features(0))
+    run = lambda cm: D.search_plans(p.model, t, f, x, K=a.K, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan, comm=cm)
+res = run(comm)
 assign = res["assign"].cpu().numpy()
 ok = True
 if rank == 0:
-    ref = D.search_plans(p.model, t, f, x, K=a.K, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan, comm=None)
+    ref = run(None)
     ok = (res["makespan"], res["cand"], res["cmax"]) == (ref["makespan"], ref["cand"], ref["cmax"])
     ok = ok and bool((assign == ref["assign"].cpu().numpy()).all())
     ok = ok and res["owner_rank"] == sharding.owner_of(a.K, res["cand"], world)
+    if a.batches:
+        ok = ok and [b["makespan"] for b in res["batches"]] == [b["makespan"] for b in ref["batches"]]
 # every rank must hold the same winner and assignment
 h = torch.tensor([res["makespan"], res["cand"], int(assign.astype(np.int64).sum())], dtype=torch.int64).cuda()
 hmax, hmin = h.clone(), h.clone()
@@ -48,7 +60,8 @@ ok = ok and bool((hmax == hmin).all().item())
 flag = torch.tensor([1 if ok else 0], dtype=torch.int32).cuda()
 dist.all_reduce(flag, op=dist.ReduceOp.MIN)
 if rank == 0:
-    print(json.dumps({"world": world, "config": a.config, "K": a.K, "T": res["makespan"], "cand": res["cand"],
+    print(json.dumps({"world": world, "config": a.config, "K": a.K, "batches": a.batches, "T": res["makespan"],
+                      "cand": res["cand"],
                       "owner": res["owner_rank"], "ok": bool(flag.item())}), flush=True)
 comm.close()
 dist.destroy_process_group()
