@@ -462,6 +462,106 @@ int orc_run_candidate(const uint32_t* q, uint32_t n, const orc_plan* p, const or
     return st;
 }
 
+/* ------------------------------------------------------------------------- */
+/* N3: exact C_max by branch and bound, see the header.            */
+/* ------------------------------------------------------------------------- */
+typedef struct bb_state {
+    const uint32_t* q;
+    uint32_t n, m;
+    const uint32_t* pi;       /* base order: items are placed in this order   */
+    uint64_t* E;              /* [m] current encoder loads                    */
+    uint64_t* L;              /* [m] current LLM loads                        */
+    uint32_t* a;              /* [n] current assignment (by item)             */
+    uint32_t* best;           /* [n] incumbent assignment                     */
+    uint64_t incumbent, lb, nodes, budget;
+    int stop, out_of_budget;
+} bb_state;
+
+static void bb_dfs(bb_state* st, uint32_t t, uint32_t used, uint64_t curmax) {
+    if (st->stop) return;
+    if (t == st->n) { /* leaf: pruning guarantees curmax < incumbent */
+        st->incumbent = curmax;
+        memcpy(st->best, st->a, sizeof(uint32_t) * st->n);
+        if (st->incumbent <= st->lb) st->stop = 1;
+        return;
+    }
+    uint32_t i = st->pi[t];
+    uint64_t e = item_e(st->q, st->n, i), l = item_l(st->q, st->n, i);
+    uint32_t lim = used < st->m ? used + 1 : st->m; /* first-use symmetry breaking */
+    uint64_t w[256];
+    uint32_t js[256];
+    for (uint32_t j = 0; j < lim; j++) { /* children sorted by (resulting max, j): insertion */
+        uint64_t v = max64(st->E[j] + e, st->L[j] + l);
+        uint32_t k = j;
+        while (k > 0 && w[k - 1] > v) { w[k] = w[k - 1]; js[k] = js[k - 1]; k--; }
+        w[k] = v;
+        js[k] = j;
+    }
+    for (uint32_t k = 0; k < lim && !st->stop; k++) {
+        if (st->nodes >= st->budget) { st->stop = 1; st->out_of_budget = 1; return; }
+        st->nodes++;
+        uint64_t nm = max64(curmax, w[k]);
+        if (max64(nm, st->lb) >= st->incumbent) continue; /* cannot beat the incumbent */
+        uint32_t j = js[k];
+        st->E[j] += e; st->L[j] += l; st->a[i] = j;
+        bb_dfs(st, t + 1, j + 1 > used ? j + 1 : used, nm);
+        st->E[j] -= e; st->L[j] -= l;
+    }
+}
+
+int orc_exact_cmax(const uint32_t* q, uint32_t n, uint32_t m, uint64_t node_budget,
+                   const uint32_t* init_assign, uint32_t* assign_out, uint64_t* cmax, uint64_t* lower_bound,
+                   uint32_t* proven, uint64_t* nodes) {
+    if (m == 0 || m > 256) return ORC_INVALID;
+    bb_state st;
+    memset(&st, 0, sizeof st);
+    st.q = q; st.n = n; st.m = m; st.budget = node_budget;
+    uint32_t* pi = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+    st.E = (uint64_t*)calloc(m, sizeof(uint64_t));
+    st.L = (uint64_t*)calloc(m, sizeof(uint64_t));
+    st.a = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
+    st.best = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
+    orc_base_order(q, n, pi);
+    st.pi = pi;
+    /* lower bound: averages per module and the largest single item */
+    uint64_t se = 0, sl = 0, big = 0;
+    for (uint32_t i = 0; i < n; i++) {
+        uint64_t e = item_e(q, n, i), l = item_l(q, n, i);
+        se += e; sl += l; big = max64(big, max64(e, l));
+    }
+    st.lb = max64(max64((se + m - 1) / m, (sl + m - 1) / m), big);
+    /* initial incumbent */
+    uint64_t* E0 = (uint64_t*)calloc(m, sizeof(uint64_t));
+    uint64_t* L0 = (uint64_t*)calloc(m, sizeof(uint64_t));
+    if (init_assign) {
+        for (uint32_t i = 0; i < n; i++) {
+            if (init_assign[i] >= m) { free(E0); free(L0); free(pi); free(st.E); free(st.L); free(st.a); free(st.best); return ORC_INVALID; }
+            st.best[i] = init_assign[i];
+        }
+    } else { /* the paper's LPT: lowest current max(E_j, L_j), lowest j */
+        for (uint32_t t = 0; t < n; t++) {
+            uint32_t i = pi[t], bj = 0;
+            for (uint32_t j = 1; j < m; j++)
+                if (max64(E0[j], L0[j]) < max64(E0[bj], L0[bj])) bj = j;
+            E0[bj] += item_e(q, n, i); L0[bj] += item_l(q, n, i);
+            st.best[i] = bj;
+        }
+        memset(E0, 0, sizeof(uint64_t) * m); memset(L0, 0, sizeof(uint64_t) * m);
+    }
+    for (uint32_t i = 0; i < n; i++) { E0[st.best[i]] += item_e(q, n, i); L0[st.best[i]] += item_l(q, n, i); }
+    st.incumbent = 0;
+    for (uint32_t j = 0; j < m; j++) st.incumbent = max64(st.incumbent, max64(E0[j], L0[j]));
+    free(E0); free(L0);
+    if (st.incumbent > st.lb && n > 0) bb_dfs(&st, 0, 0, 0);
+    *cmax = st.incumbent;
+    *lower_bound = st.lb;
+    *proven = (st.incumbent <= st.lb || !st.out_of_budget) ? 1u : 0u;
+    *nodes = st.nodes;
+    if (assign_out) memcpy(assign_out, st.best, sizeof(uint32_t) * n);
+    free(pi); free(st.E); free(st.L); free(st.a); free(st.best);
+    return ORC_OK;
+}
+
 int orc_balance(const uint32_t* q, uint32_t n, const orc_plan* p, const orc_bparams* bp, uint32_t c0,
                 uint32_t c1, uint64_t* cand_T, uint64_t* cand_cmax, uint64_t* best_T, uint32_t* best_c,
                 uint64_t* best_cmax, uint32_t* best_assign) {

@@ -131,6 +131,18 @@ int orc_balance(const uint32_t* cost_q, uint32_t n, const orc_plan* p, const orc
                 uint32_t c0, uint32_t c1, uint64_t* cand_T, uint64_t* cand_cmax,
                 uint64_t* best_T, uint32_t* best_c, uint64_t* best_cmax, uint32_t* best_assign);
 
+/* N3 exact C_max (P:703-727 ILP objective; S:390-398 solve_exact): node-budgeted
+ * branch and bound over item -> bucket assignments, items in the base order pi, children
+ * in (resulting max(E_j + e, L_j + l), j) order, bucket first-use symmetry breaking (an
+ * item may open only the lowest unused bucket), prune when max(node max, LB) >= incumbent.
+ * LB = max(ceil(sum e / m), ceil(sum l / m), max_i max(e_i, l_i)).  The incumbent starts
+ * from init_assign (its C_max) or, if NULL, from the paper's LPT (current-load rule).
+ * proven = the search finished within node_budget child visits (or incumbent == LB).
+ * assign_out[n] (may be NULL) receives the best assignment found. */
+int orc_exact_cmax(const uint32_t* cost_q, uint32_t n, uint32_t m, uint64_t node_budget,
+                   const uint32_t* init_assign, uint32_t* assign_out, uint64_t* cmax, uint64_t* lower_bound,
+                   uint32_t* proven, uint64_t* nodes);
+
 /* CSR index groups ("returns a set of index groups"): bucket-major, items ascending. */
 void orc_groups(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items);
 

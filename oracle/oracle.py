@@ -86,6 +86,7 @@ def lib():
         L.orc_predict.argtypes = [P(OrcModel), P(OrcPlan), u32p, u32p, u32p, C.c_uint32, f64p, u32p, u32p]
         L.orc_predict_corrected.argtypes = [P(OrcModel), P(OrcPlan), u32p, u32p, u32p, C.c_uint32, f64p, f64p,
                                             u32p, u32p]
+        L.orc_exact_cmax.argtypes = [u32p, C.c_uint32, C.c_uint32, C.c_uint64, u32p, u32p, u64p, u64p, u32p, u64p]
         L.orc_shape_bin.argtypes = [C.c_uint64]
         L.orc_shape_bin.restype = C.c_uint32
         L.orc_base_order.argtypes = [u32p, C.c_uint32, u32p]
@@ -432,3 +433,19 @@ def expected_makespan_choice(plans, batch_costs, K, R, G, seed, threads=None):
         per.append(rows)
     win = min(range(len(plans)), key=lambda p: (sums[p], p))
     return win, sums, per
+
+
+def exact_cmax(cost_q, m, node_budget=10 ** 7, init_assign=None):
+    """N3 branch and bound: dict(cmax, lb, proven, nodes, assign)."""
+    q = _u32(cost_q)
+    n = q.shape[1]
+    a = np.zeros(max(n, 1), np.uint32)
+    ia = None if init_assign is None else np.ascontiguousarray(np.asarray(init_assign, np.uint32))
+    cm, lb, nodes = np.zeros(1, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+    pr = np.zeros(1, np.uint32)
+    st = lib().orc_exact_cmax(_p(q, C.c_uint32), n, m, int(node_budget), None if ia is None else _p(ia, C.c_uint32),
+                              _p(a, C.c_uint32), _p(cm, C.c_uint64), _p(lb, C.c_uint64), _p(pr, C.c_uint32),
+                              _p(nodes, C.c_uint64))
+    if st != 0:
+        raise ValueError(f"orc_exact_cmax status {st}")
+    return dict(cmax=int(cm[0]), lb=int(lb[0]), proven=bool(pr[0]), nodes=int(nodes[0]), assign=a[:n])

@@ -120,3 +120,27 @@ def opt_cmax_1d(loads: Sequence[int], m: int) -> int:
         v = max(sums)
         best = v if best is None else min(best, v)
     return best
+
+
+def opt_cmax_2d(cost, m: int) -> int:
+    """min over all m^n assignments of max_j max(E_j, L_j), E = ef + eb, L = lf + lb."""
+    n = len(cost[0])
+    e = [int(cost[0][i]) + int(cost[1][i]) for i in range(n)]
+    l = [int(cost[2][i]) + int(cost[3][i]) for i in range(n)]
+    best = None
+    for a in itertools.product(range(m), repeat=n):
+        E, L = [0] * m, [0] * m
+        for i, j in enumerate(a):
+            E[j] += e[i]
+            L[j] += l[i]
+        v = max(max(E), max(L))
+        best = v if best is None else min(best, v)
+    return best
+
+
+def cmax_of(assign, cost, m: int) -> int:
+    E, L = [0] * m, [0] * m
+    for i, j in enumerate(assign):
+        E[j] += int(cost[0][i]) + int(cost[1][i])
+        L[j] += int(cost[2][i]) + int(cost[3][i])
+    return max(max(E), max(L))

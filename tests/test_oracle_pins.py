@@ -578,3 +578,37 @@ def test_expected_makespan_argmin_and_ties(O):
     assert win == min(range(2), key=lambda p: (sums[p], p))
     # brute force over the sums
     assert sums[win] == min(sums)
+
+
+# ------------------------------------------------------------------ N3 exact C_max (B&B)
+def test_exact_spec_examples(O):
+    r = O.exact_cmax(loads_1d([8, 7, 6, 5, 4]), 2)                      # S:394 -> 15
+    assert r["proven"] and r["cmax"] == 15 and BF.cmax_of(r["assign"], loads_1d([8, 7, 6, 5, 4]), 2) == 15
+    c = np.zeros((4, 1), np.uint32); c[0], c[2] = 3, 9                    # S:395 single item, m = 1
+    r = O.exact_cmax(c, 1)
+    assert r["proven"] and r["cmax"] == 9
+    r = O.exact_cmax(loads_1d([6, 6]), 2)                                 # S:396 one per bucket
+    assert r["proven"] and r["cmax"] == 6 and sorted(r["assign"]) == [0, 1]
+    r = O.exact_cmax(loads_1d([3, 3, 2, 2, 2]), 2)                        # Graham-tight: LPT 7, optimum 6
+    assert r["proven"] and r["cmax"] == 6
+
+
+def test_exact_matches_bruteforce_2d(O):
+    rng = np.random.default_rng(31)
+    for trial in range(40):
+        n, m = int(rng.integers(1, 8)), int(rng.integers(1, 4))
+        c = rng.integers(0, 30, (4, n)).astype(np.uint32)
+        r = O.exact_cmax(c, m)
+        assert r["proven"] and r["cmax"] == BF.opt_cmax_2d(c, m), (trial, n, m)
+        assert BF.cmax_of(r["assign"], c, m) == r["cmax"] and r["lb"] <= r["cmax"]
+
+
+def test_exact_budget_and_incumbent(O):
+    rng = np.random.default_rng(7)
+    c = rng.integers(1, 1000, (4, 9)).astype(np.uint32)
+    opt = BF.opt_cmax_2d(c, 3)
+    r = O.exact_cmax(c, 3, node_budget=3)                                 # stopped early: a valid bound
+    assert r["nodes"] <= 3 and r["cmax"] >= opt and BF.cmax_of(r["assign"], c, 3) == r["cmax"]
+    assert r["proven"] == (r["cmax"] == r["lb"])
+    full = O.exact_cmax(c, 3, init_assign=r["assign"])                    # warm start: same optimum
+    assert full["proven"] and full["cmax"] == opt
