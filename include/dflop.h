@@ -329,6 +329,37 @@ dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_cost_model*
                                 dflop_plan_result* out, uint32_t* assign, uint64_t* stage_a_out,
                                 uint64_t stage_a_cap, dflop_stream_t stream);
 
+/* ---------------------------------------------------------------- N3 exact C_max
+ * The ILP of P:703-727 (minimise C_max = max_j max(E_j, L_j) over assignments of the n
+ * samples to m = N_mb * L_dp buckets), solved by a node-budgeted parallel branch and bound
+ * (SPEC solve_exact): items in the LPT base order, first-use symmetry breaking,
+ * lower bound LB = max(ceil(sum e / m), ceil(sum l / m), max_i max(e_i, l_i)).  The
+ * incumbent starts from init_assign (e.g. the search's winner) or the paper's LPT.  The
+ * result is a C_max certificate (proven, or the gap to LB) and an extra candidate: its
+ * assignment scored by the 1F1B simulation (makespan). */
+typedef struct dflop_exact_result {
+    uint32_t struct_size;
+    uint32_t proven;      /* 1: cmax is the optimum (search finished or cmax == LB)     */
+    uint64_t cmax;        /* best C_max found, ticks                                     */
+    uint64_t lower_bound; /* LB, ticks                                                   */
+    uint64_t nodes;       /* child visits                                                */
+    uint64_t makespan;    /* 1F1B makespan of the returned assignment (max over replicas) */
+    uint32_t searched;    /* 1: the tree search ran (n <= 256, m <= 32); 0: bound only    */
+    uint32_t reserved;
+} dflop_exact_result;
+
+/* cost_ticks  device u32 [4][n] (ef, eb, lf, lb); n <= 65535.
+ * plan        host; m = n_mb * l_dp <= 256.
+ * node_budget child visits over the whole search (split over the parallel subtrees).
+ * init_assign device u32 [n] or NULL (bucket per sample, < m).
+ * ws/ws_bytes workspace query as in dflop_balance_microbatches.
+ * out         host result; assign: device u32 [n] or NULL (the returned assignment).
+ * Synchronous.  Errors: INVALID_ARGUMENT (plan, m > 256, an init_assign entry >= m),
+ * SHAPE (n > 65535), WORKSPACE_TOO_SMALL, CUDA. */
+dflop_status dflop_exact_cmax(const uint32_t* cost_ticks, uint32_t n, const dflop_plan* plan, uint64_t node_budget,
+                              const uint32_t* init_assign, void* ws, size_t* ws_bytes, dflop_exact_result* out,
+                              uint32_t* assign, dflop_stream_t stream);
+
 /* ---------------------------------------------------------------- N2 search over a sample
  * Eq. (1): theta* = argmin_theta (1/|D|) sum_{d in D} T(d; theta) over a sample
  * of D global batches, each balanced and scored on the device exactly as in

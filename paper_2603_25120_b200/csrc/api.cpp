@@ -875,6 +875,35 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
 
 }  // namespace dflop
 
+extern "C" dflop_status dflop_exact_cmax(const uint32_t* cost_ticks, uint32_t n, const dflop_plan* plan,
+                                         uint64_t node_budget, const uint32_t* init_assign, void* ws, size_t* ws_bytes,
+                                         dflop_exact_result* out, uint32_t* assign, dflop_stream_t stream) {
+    g_err.clear();
+    dflop_status st = validate_plan(plan);
+    if (st != DFLOP_OK) return st;
+    const uint32_t m = plan->n_mb * plan->l_dp;
+    if (m > 256) return invalid("exact solver: m = %u > 256", m);
+    if (plan->e_pp + plan->l_pp > 32) return invalid("S = E_pp + L_pp must be <= 32");
+    if (n > 65535) {
+        set_error("n=%u > 65535", n);
+        return DFLOP_ERR_SHAPE;
+    }
+    if (n > 0 && !cost_ticks) return invalid("cost_ticks is NULL");
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    const size_t need = exact_ws_bytes(n, m, plan);
+    if (!ws) {
+        *ws_bytes = need;
+        return DFLOP_OK;
+    }
+    if (*ws_bytes < need) {
+        set_error("workspace %zu B < required %zu B", *ws_bytes, need);
+        return DFLOP_ERR_WORKSPACE_TOO_SMALL;
+    }
+    if ((uintptr_t)ws % 256) return invalid("workspace must be 256-byte aligned");
+    if (!out) return invalid("out is NULL");
+    return exact_launch(cost_ticks, n, plan, node_budget, init_assign, ws, out, assign, (cudaStream_t)stream);
+}
+
 extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_cost_model* cm,
                                            const dflop_mem_model* mm, const uint32_t* tiles, const uint32_t* frames,
                                            const uint32_t* text, uint32_t n, const dflop_search_params* sp,

@@ -107,6 +107,18 @@ dflop_status simulate_launch(const uint64_t* fwd, const uint64_t* bwd, uint32_t 
                              uint64_t* makespan, uint64_t* busy, const SlotProgram& prog, cudaStream_t s);
 
 size_t groups_ws_bytes(uint32_t n, uint32_t m);
+
+#ifdef __CUDACC__
+// a2 kernels shared by the balance and the exact solver (balance.cu; types from common.cuh)
+__global__ void k_prep_keys(const uint32_t* __restrict__ cost, uint32_t n, size_t rs, BalanceHeader* hdr, u64* keys);
+__global__ void k_rank_sort(const u64* __restrict__ keys, uint32_t n, uint32_t* order, uint32_t* item_pos);
+#endif
+
+// ---------------------------------------------------------------- N3 exact C_max (exact.cu)
+size_t exact_ws_bytes(uint32_t n, uint32_t m, const dflop_plan* p);
+dflop_status exact_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p, uint64_t node_budget,
+                          const uint32_t* init_assign, void* ws, dflop_exact_result* out, uint32_t* assign,
+                          cudaStream_t s);
 cudaError_t groups_launch(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items,
                           void* ws, cudaStream_t s);
 

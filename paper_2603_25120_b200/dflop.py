@@ -26,7 +26,7 @@ STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE", 3: "OVERFLOW", 4: "INFEASI
 EXPORTS = ["dflop_abi_version", "dflop_last_error", "dflop_release_caches", "dflop_predict_costs",
            "dflop_balance_microbatches", "dflop_simulate_1f1b", "dflop_index_groups", "dflop_search_plans",
            "dflop_get_unique_id", "dflop_comm_init", "dflop_comm_destroy", "dflop_profile_enable",
-           "dflop_profile_read", "dflop_search_plans_batches"]
+           "dflop_profile_read", "dflop_search_plans_batches", "dflop_exact_cmax"]
 
 
 class DflopError(RuntimeError):
@@ -47,6 +47,13 @@ class MemGrid(C.Structure):
 
 
 CORR_BINS = 32
+
+
+class ExactResult(C.Structure):
+    """dflop_exact_result (N3)."""
+    _fields_ = [("struct_size", C.c_uint32), ("proven", C.c_uint32), ("cmax", C.c_uint64),
+                ("lower_bound", C.c_uint64), ("nodes", C.c_uint64), ("makespan", C.c_uint64),
+                ("searched", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class Correction(C.Structure):
@@ -380,6 +387,32 @@ def search_plans(model: Dict, tiles, frames, text, K: int, R: int, G: int, seed:
     r["plan"] = out.plan.as_dict()
     r["alg1_plan"] = out.alg1_plan.as_dict()
     r["assign"] = assign[:n] if assign is not None else None
+    return r
+
+
+def exact_cmax(cost_ticks, plan: Dict, node_budget: int = 10 ** 9, init_assign=None,
+               ws: Optional[Workspace] = None, stream=None) -> Dict:
+    """N3: exact C_max by branch and bound (synchronous).  Returns the dflop_exact_result
+    fields and 'assign' (device int32 [n])."""
+    import torch
+    n = cost_ticks.shape[1]
+    dev = cost_ticks.device
+    ps = plan_struct(plan)
+    L = lib()
+    need = C.c_size_t(0)
+    out = ExactResult()
+    _check(L.dflop_exact_cmax(_ptr(cost_ticks), n, C.byref(ps), C.c_uint64(int(node_budget)), None, None,
+                              C.byref(need), C.byref(out), None, None))
+    wsb = (ws or _default_ws).get(need.value, dev)
+    have = C.c_size_t(wsb.numel())
+    assign = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _check(L.dflop_exact_cmax(_ptr(cost_ticks), n, C.byref(ps), C.c_uint64(int(node_budget)),
+                              _ptr(init_assign) if init_assign is not None else None, _ptr(wsb), C.byref(have),
+                              C.byref(out), _ptr(assign), _stream(stream)))
+    r = {f: getattr(out, f) for f, _ in ExactResult._fields_ if f not in ("struct_size", "reserved")}
+    r["proven"] = bool(r["proven"])
+    r["searched"] = bool(r["searched"])
+    r["assign"] = assign[:n]
     return r
 
 

@@ -27,7 +27,7 @@ def declared_functions():
 
 def test_exports_every_declared_symbol(D):
     names = declared_functions()
-    assert len(names) == 14
+    assert len(names) == 15
     assert sorted(names) == sorted(D.EXPORTS)
     out = subprocess.run(["nm", "-D", "--defined-only", D.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (dflop_\w+)", out))
@@ -63,7 +63,7 @@ PROBE = r"""
 int main(void) {
   S(dflop_grid) S(dflop_mem_grid) S(dflop_cost_model) S(dflop_mem_model) S(dflop_plan) S(dflop_cluster)
   S(dflop_balance_params) S(dflop_cand_result) S(dflop_search_params) S(dflop_plan_result) S(dflop_profile)
-  S(dflop_correction) F(dflop_correction, rho)
+  S(dflop_correction) F(dflop_correction, rho) S(dflop_exact_result) F(dflop_exact_result, makespan)
   F(dflop_cost_model, bwd_ratio) F(dflop_cost_model, thr_e) F(dflop_cost_model, thr_lin)
   F(dflop_cost_model, correction)
   F(dflop_mem_model, ms_e) F(dflop_mem_model, mem_per_gpu) F(dflop_balance_params, id_base)
@@ -84,7 +84,7 @@ def test_struct_layouts_match_header(D, tmp_path):
          "dflop_mem_model": D.MemModel, "dflop_plan": D.Plan, "dflop_cluster": D.Cluster,
          "dflop_balance_params": D.BalanceParams, "dflop_cand_result": D.CandResult,
          "dflop_search_params": D.SearchParams, "dflop_plan_result": D.PlanResult, "dflop_profile": D.Profile,
-         "dflop_correction": D.Correction}
+         "dflop_correction": D.Correction, "dflop_exact_result": D.ExactResult}
     for k, v in got.items():
         if "." in k:
             s, f = k.split(".")
