@@ -562,6 +562,95 @@ int orc_exact_cmax(const uint32_t* q, uint32_t n, uint32_t m, uint64_t node_budg
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------- */
+/* N4(a): microbatch-order search per replica (see the header).                */
+/* ------------------------------------------------------------------------- */
+static uint64_t order_makespan(const bucket_sums* bk, const orc_plan* p, uint32_t rho, const uint32_t* ord,
+                               uint64_t* F, uint64_t* B) {
+    uint32_t S = p->e_pp + p->l_pp, M = p->n_mb;
+    for (uint32_t s = 0; s < S; s++)
+        for (uint32_t k = 0; k < M; k++) {
+            const bucket_sums* b = &bk[ord[k] * p->l_dp + rho];
+            F[s * M + k] = s < p->e_pp ? b->EF : b->LF;
+            B[s * M + k] = s < p->e_pp ? b->EB : b->LB;
+        }
+    uint64_t T = 0;
+    orc_simulate_1f1b(F, B, S, M, &T, NULL);
+    return T;
+}
+
+int orc_order_search(const uint32_t* q, uint32_t n, const orc_plan* p, const uint32_t* assign, uint32_t rounds,
+                     uint32_t* order_out, uint64_t* T_out) {
+    uint32_t m = p->n_mb * p->l_dp, M = p->n_mb, S = p->e_pp + p->l_pp;
+    bucket_sums* bk = (bucket_sums*)calloc(m, sizeof(bucket_sums));
+    for (uint32_t i = 0; i < n; i++) {
+        if (assign[i] >= m) { free(bk); return ORC_INVALID; }
+        add_item(&bk[assign[i]], q, n, i);
+    }
+    uint64_t* F = (uint64_t*)malloc(sizeof(uint64_t) * S * M);
+    uint64_t* B = (uint64_t*)malloc(sizeof(uint64_t) * S * M);
+    uint32_t* cand = (uint32_t*)malloc(sizeof(uint32_t) * M);
+    uint32_t* ord = (uint32_t*)malloc(sizeof(uint32_t) * M);
+    uint64_t* W = (uint64_t*)malloc(sizeof(uint64_t) * M);
+    uint32_t* asc = (uint32_t*)malloc(sizeof(uint32_t) * M);
+    for (uint32_t rho = 0; rho < p->l_dp; rho++) {
+        for (uint32_t k = 0; k < M; k++) {
+            const bucket_sums* b = &bk[k * p->l_dp + rho];
+            W[k] = max64(bE(b), bL(b));
+            asc[k] = k;
+        }
+        /* stable insertion sort of the slots by W ascending */
+        for (uint32_t a = 1; a < M; a++) {
+            uint32_t x = asc[a], b = a;
+            while (b > 0 && W[asc[b - 1]] > W[x]) { asc[b] = asc[b - 1]; b--; }
+            asc[b] = x;
+        }
+        uint64_t bestT = 0;
+        for (uint32_t o = 0; o < 4; o++) {
+            if (o == 0) for (uint32_t k = 0; k < M; k++) cand[k] = k;
+            if (o == 1) for (uint32_t k = 0; k < M; k++) cand[k] = asc[k];
+            if (o == 2) { /* descending W, ties by slot ascending */
+                uint32_t k = 0;
+                for (uint32_t e = M; e > 0;) {
+                    uint32_t s0 = e - 1; /* run of equal W ending at e-1 in asc */
+                    while (s0 > 0 && W[asc[s0 - 1]] == W[asc[e - 1]]) s0--;
+                    for (uint32_t t = s0; t < e; t++) cand[k++] = asc[t];
+                    e = s0;
+                }
+            }
+            if (o == 3) { /* valley */
+                uint32_t lo = 0, hi = M - 1;
+                for (uint32_t t = 0; t < M; t++) {
+                    if (t % 2 == 0) cand[lo++] = asc[t];
+                    else cand[hi--] = asc[t];
+                }
+            }
+            uint64_t T = order_makespan(bk, p, rho, cand, F, B);
+            if (o == 0 || T < bestT) { bestT = T; memcpy(ord, cand, sizeof(uint32_t) * M); }
+        }
+        for (uint32_t r = 0; r < rounds; r++) {
+            uint64_t rT = 0;
+            uint32_t ra = 0, rb = 0;
+            int found = 0;
+            for (uint32_t a = 0; a < M; a++)
+                for (uint32_t b = a + 1; b < M; b++) {
+                    if (M > 128 && b - a > 16) break;
+                    uint32_t t = ord[a]; ord[a] = ord[b]; ord[b] = t;
+                    uint64_t T = order_makespan(bk, p, rho, ord, F, B);
+                    t = ord[a]; ord[a] = ord[b]; ord[b] = t;
+                    if (!found || T < rT) { found = 1; rT = T; ra = a; rb = b; } /* (T, a, b) order */
+                }
+            if (!found || rT >= bestT) break;
+            uint32_t t = ord[ra]; ord[ra] = ord[rb]; ord[rb] = t;
+            bestT = rT;
+        }
+        for (uint32_t k = 0; k < M; k++) order_out[rho * M + k] = ord[k] * p->l_dp + rho;
+        T_out[rho] = bestT;
+    }
+    free(bk); free(F); free(B); free(cand); free(ord); free(W); free(asc);
+    return ORC_OK;
+}
+
 int orc_balance(const uint32_t* q, uint32_t n, const orc_plan* p, const orc_bparams* bp, uint32_t c0,
                 uint32_t c1, uint64_t* cand_T, uint64_t* cand_cmax, uint64_t* best_T, uint32_t* best_c,
                 uint64_t* best_cmax, uint32_t* best_assign) {

@@ -143,6 +143,18 @@ int orc_exact_cmax(const uint32_t* cost_q, uint32_t n, uint32_t m, uint64_t node
                    const uint32_t* init_assign, uint32_t* assign_out, uint64_t* cmax, uint64_t* lower_bound,
                    uint32_t* proven, uint64_t* nodes);
 
+/* N4(a) microbatch-order search (R11: the 1F1B makespan depends on the slot order; SURVEY
+ * 8(f) N4).  For each LLM replica rho (buckets j = k * L_dp + rho, slot k by default, R10)
+ * independently: start from the best of four orders -- 0 identity, 1 ascending W_j =
+ * max(E_j, L_j), 2 descending W_j, 3 valley (ascending W placed alternately at the front and
+ * the back, the largest in the middle); ties by (makespan, order index), sorts stable by
+ * slot -- then best-improvement pairwise swaps of slot positions (a < b; every pair when
+ * M <= 128, else b - a <= 16), the lexicographic minimum of (makespan, a, b), applied while
+ * it is strictly better, at most `rounds` times (R35).  order_out[rho * M + k] = bucket of
+ * slot k; T_out[rho] = its makespan.  T of the plan = max over replicas. */
+int orc_order_search(const uint32_t* cost_q, uint32_t n, const orc_plan* p, const uint32_t* assign,
+                     uint32_t rounds, uint32_t* order_out, uint64_t* T_out);
+
 /* CSR index groups ("returns a set of index groups"): bucket-major, items ascending. */
 void orc_groups(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items);
 

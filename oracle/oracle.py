@@ -87,6 +87,7 @@ def lib():
         L.orc_predict_corrected.argtypes = [P(OrcModel), P(OrcPlan), u32p, u32p, u32p, C.c_uint32, f64p, f64p,
                                             u32p, u32p]
         L.orc_exact_cmax.argtypes = [u32p, C.c_uint32, C.c_uint32, C.c_uint64, u32p, u32p, u64p, u64p, u32p, u64p]
+        L.orc_order_search.argtypes = [u32p, C.c_uint32, P(OrcPlan), u32p, C.c_uint32, u32p, u64p]
         L.orc_shape_bin.argtypes = [C.c_uint64]
         L.orc_shape_bin.restype = C.c_uint32
         L.orc_base_order.argtypes = [u32p, C.c_uint32, u32p]
@@ -449,3 +450,18 @@ def exact_cmax(cost_q, m, node_budget=10 ** 7, init_assign=None):
     if st != 0:
         raise ValueError(f"orc_exact_cmax status {st}")
     return dict(cmax=int(cm[0]), lb=int(lb[0]), proven=bool(pr[0]), nodes=int(nodes[0]), assign=a[:n])
+
+
+def order_search(cost_q, plan: Dict, assign, rounds=64):
+    """N4(a): per replica the slot order (bucket per slot) and its 1F1B makespan."""
+    q = _u32(cost_q)
+    n = q.shape[1]
+    a = np.ascontiguousarray(np.asarray(assign, np.uint32))
+    M, rep = plan["n_mb"], plan["l_dp"]
+    order = np.zeros(M * rep, np.uint32)
+    T = np.zeros(rep, np.uint64)
+    st = lib().orc_order_search(_p(q, C.c_uint32), n, C.byref(plan_struct(plan)), _p(a, C.c_uint32), rounds,
+                                _p(order, C.c_uint32), _p(T, C.c_uint64))
+    if st != 0:
+        raise ValueError(f"orc_order_search status {st}")
+    return order.reshape(rep, M), T

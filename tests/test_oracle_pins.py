@@ -612,3 +612,45 @@ def test_exact_budget_and_incumbent(O):
     assert r["proven"] == (r["cmax"] == r["lb"])
     full = O.exact_cmax(c, 3, init_assign=r["assign"])                    # warm start: same optimum
     assert full["proven"] and full["cmax"] == opt
+
+
+# ------------------------------------------------------------------ N4(a) microbatch order
+def test_order_search_survey_counterexample(O):
+    # F = [[1,5],[5,1]], B = 2F gives 29 in slot order, 25 reversed
+    c = np.zeros((4, 2), np.uint32)
+    c[0], c[1], c[2], c[3] = [1, 5], [2, 10], [5, 1], [10, 2]
+    pl = plan(n_mb=2)
+    T_id, _ = O.simulate_1f1b(np.array([[1, 5], [5, 1]], np.uint64), np.array([[2, 10], [10, 2]], np.uint64))
+    assert T_id == 29
+    order, T = O.order_search(c, pl, [0, 1])
+    assert int(T[0]) == 25 and list(order[0]) == [1, 0]
+
+
+def test_order_search_bounds_vs_bruteforce(O):
+    import itertools
+    rng = np.random.default_rng(3)
+    for trial in range(25):
+        M, e_pp, l_pp = int(rng.integers(1, 6)), int(rng.integers(1, 3)), int(rng.integers(1, 3))
+        c = rng.integers(1, 60, (4, M)).astype(np.uint32)
+        pl = plan(e_pp=e_pp, l_pp=l_pp, n_mb=M)
+        order, T = O.order_search(c, pl, list(range(M)))
+        S = e_pp + l_pp
+        def sim(o):
+            F = np.array([[c[0 if s < e_pp else 2][o[k]] for k in range(M)] for s in range(S)], np.uint64)
+            B = np.array([[c[1 if s < e_pp else 3][o[k]] for k in range(M)] for s in range(S)], np.uint64)
+            return O.simulate_1f1b(F, B)[0]
+        best = min(sim(o) for o in itertools.permutations(range(M)))
+        assert sim(list(order[0])) == int(T[0]) and best <= int(T[0]) <= sim(list(range(M)))
+        assert sorted(order[0]) == list(range(M))
+        if M <= 2:
+            assert int(T[0]) == best
+
+
+def test_order_search_uniform_and_replicas(O):
+    c = np.full((4, 12), 3, np.uint32)
+    pl = plan(e_pp=2, l_pp=3, n_mb=4, l_dp=3)
+    a = [i % 12 for i in range(12)]
+    order, T = O.order_search(c, pl, a)
+    assert (T == (4 + 5 - 1) * 6).all()                          # uniform: 1F1B closed form
+    for rho in range(3):                                           # identity kept on ties
+        assert list(order[rho]) == [k * 3 + rho for k in range(4)]
