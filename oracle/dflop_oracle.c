@@ -651,6 +651,47 @@ int orc_order_search(const uint32_t* q, uint32_t n, const orc_plan* p, const uin
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------- */
+/* N4(b): inter-model routing plan (see the header).                          */
+/* ------------------------------------------------------------------------- */
+int orc_route_plan(const uint32_t* q, uint32_t n, const orc_plan* p, const uint32_t* assign, uint32_t* pos_item,
+                   uint32_t* slot_off, uint32_t* enc_off, uint32_t* llm_off, uint64_t* enc_load) {
+    uint32_t M = p->n_mb, R = p->l_dp, G = p->e_dp, m = M * R;
+    for (uint32_t i = 0; i < n; i++)
+        if (assign[i] >= m) return ORC_INVALID;
+    uint32_t t = 0;
+    for (uint32_t k = 0; k < M; k++) {
+        slot_off[k] = t;
+        for (uint32_t rho = 0; rho < R; rho++) {
+            llm_off[k * (R + 1) + rho] = t;
+            for (uint32_t i = 0; i < n; i++) /* bucket members, sample index ascending */
+                if (assign[i] == k * R + rho) pos_item[t++] = i;
+        }
+        llm_off[k * (R + 1) + R] = t;
+        uint32_t a = slot_off[k], b = t;
+        uint64_t tot = 0;
+        for (uint32_t u = a; u < b; u++) tot += item_e(q, n, pos_item[u]);
+        enc_off[k * (G + 1)] = a;
+        for (uint32_t g = 1; g < G; g++) {
+            /* first position whose preceding encoder cost reaches g/G of the slot's */
+            uint64_t pre = 0;
+            uint32_t u = a;
+            while (u < b && pre * G < (uint64_t)g * tot) pre += item_e(q, n, pos_item[u++]);
+            enc_off[k * (G + 1) + g] = u;
+        }
+        enc_off[k * (G + 1) + G] = b;
+        if (enc_load)
+            for (uint32_t g = 0; g < G; g++) {
+                uint64_t s = 0;
+                for (uint32_t u = enc_off[k * (G + 1) + g]; u < enc_off[k * (G + 1) + g + 1]; u++)
+                    s += item_e(q, n, pos_item[u]);
+                enc_load[k * G + g] = s;
+            }
+    }
+    slot_off[M] = t;
+    return ORC_OK;
+}
+
 int orc_balance(const uint32_t* q, uint32_t n, const orc_plan* p, const orc_bparams* bp, uint32_t c0,
                 uint32_t c1, uint64_t* cand_T, uint64_t* cand_cmax, uint64_t* best_T, uint32_t* best_c,
                 uint64_t* best_cmax, uint32_t* best_assign) {

@@ -155,6 +155,18 @@ int orc_exact_cmax(const uint32_t* cost_q, uint32_t n, uint32_t m, uint64_t node
 int orc_order_search(const uint32_t* cost_q, uint32_t n, const orc_plan* p, const uint32_t* assign,
                      uint32_t rounds, uint32_t* order_out, uint64_t* T_out);
 
+/* N4(b) inter-model routing plan (Fig. "inter_model_comm"): for microbatch slot k
+ * the L_dp LLM data groups run buckets k * L_dp + rho (R10); the E_dp encoder data groups
+ * split the slot's samples -- concatenated in (rho, sample index) order -- into E_dp
+ * contiguous ranges balanced by encoder cost e_i = ef + eb: range g starts at the first
+ * position t with (sum of e before t) * E_dp >= g * (slot total) (R36).  The communicator
+ * gathers encoder range g and scatters it to the LLM ranges (forward; reversed backward).
+ * Outputs: pos_item[n] (the sample at each position, slot-major), slot_off[N_mb + 1],
+ * enc_off[N_mb][E_dp + 1] and llm_off[N_mb][L_dp + 1] (absolute positions), enc_load
+ * [N_mb][E_dp] (sum of e per encoder range; may be NULL). */
+int orc_route_plan(const uint32_t* cost_q, uint32_t n, const orc_plan* p, const uint32_t* assign,
+                   uint32_t* pos_item, uint32_t* slot_off, uint32_t* enc_off, uint32_t* llm_off, uint64_t* enc_load);
+
 /* CSR index groups ("returns a set of index groups"): bucket-major, items ascending. */
 void orc_groups(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items);
 

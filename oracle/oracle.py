@@ -88,6 +88,7 @@ def lib():
                                             u32p, u32p]
         L.orc_exact_cmax.argtypes = [u32p, C.c_uint32, C.c_uint32, C.c_uint64, u32p, u32p, u64p, u64p, u32p, u64p]
         L.orc_order_search.argtypes = [u32p, C.c_uint32, P(OrcPlan), u32p, C.c_uint32, u32p, u64p]
+        L.orc_route_plan.argtypes = [u32p, C.c_uint32, P(OrcPlan), u32p, u32p, u32p, u32p, u32p, u64p]
         L.orc_shape_bin.argtypes = [C.c_uint64]
         L.orc_shape_bin.restype = C.c_uint32
         L.orc_base_order.argtypes = [u32p, C.c_uint32, u32p]
@@ -465,3 +466,22 @@ def order_search(cost_q, plan: Dict, assign, rounds=64):
     if st != 0:
         raise ValueError(f"orc_order_search status {st}")
     return order.reshape(rep, M), T
+
+
+def route_plan(cost_q, plan: Dict, assign):
+    """N4(b): dict(pos_item, slot_off, enc_off [N_mb][E_dp+1], llm_off [N_mb][L_dp+1], enc_load)."""
+    q = _u32(cost_q)
+    n = q.shape[1]
+    a = np.ascontiguousarray(np.asarray(assign, np.uint32))
+    M, R, G = plan["n_mb"], plan["l_dp"], plan["e_dp"]
+    pos = np.zeros(max(n, 1), np.uint32)
+    so = np.zeros(M + 1, np.uint32)
+    eo = np.zeros(M * (G + 1), np.uint32)
+    lo = np.zeros(M * (R + 1), np.uint32)
+    el = np.zeros(M * G, np.uint64)
+    st = lib().orc_route_plan(_p(q, C.c_uint32), n, C.byref(plan_struct(plan)), _p(a, C.c_uint32), _p(pos, C.c_uint32),
+                              _p(so, C.c_uint32), _p(eo, C.c_uint32), _p(lo, C.c_uint32), _p(el, C.c_uint64))
+    if st != 0:
+        raise ValueError(f"orc_route_plan status {st}")
+    return dict(pos_item=pos[:n], slot_off=so, enc_off=eo.reshape(M, G + 1), llm_off=lo.reshape(M, R + 1),
+                enc_load=el.reshape(M, G))

@@ -654,3 +654,42 @@ def test_order_search_uniform_and_replicas(O):
     assert (T == (4 + 5 - 1) * 6).all()                          # uniform: 1F1B closed form
     for rho in range(3):                                           # identity kept on ties
         assert list(order[rho]) == [k * 3 + rho for k in range(4)]
+
+
+# ------------------------------------------------------------------ N4(b) routing plan
+def test_route_plan_paper_figure_and_invariants(O):
+    # P:796's figure: encoder DP = 4, LLM DP = 2.  One slot, two LLM buckets of 4 samples of
+    # equal encoder cost: the four encoder ranges are the quarters of the slot, encoder
+    # groups 0-1 feed LLM group 0 and groups 2-3 feed LLM group 1
+    pl = plan(e_dp=4, l_dp=2, n_mb=1)
+    c = np.zeros((4, 8), np.uint32); c[0] = 5
+    assign = [0, 1, 0, 1, 0, 1, 0, 1]
+    r = O.route_plan(c, pl, assign)
+    assert list(r["pos_item"]) == [0, 2, 4, 6, 1, 3, 5, 7]
+    assert list(r["llm_off"][0]) == [0, 4, 8] and list(r["enc_off"][0]) == [0, 2, 4, 6, 8]
+    assert list(r["enc_load"][0]) == [10, 10, 10, 10]
+    # invariants on random plans: a permutation, slot-major, buckets contiguous, encoder
+    # ranges nested in the slot, each boundary the first position reaching g/E_dp of the load
+    rng = np.random.default_rng(8)
+    for trial in range(30):
+        M, R, G = int(rng.integers(1, 5)), int(rng.integers(1, 4)), int(rng.integers(1, 6))
+        pl = plan(e_dp=G, l_dp=R, n_mb=M)
+        n = int(rng.integers(0, 40))
+        c = rng.integers(0, 20, (4, n)).astype(np.uint32)
+        a = rng.integers(0, M * R, n)
+        r = O.route_plan(c, pl, a)
+        assert sorted(r["pos_item"]) == list(range(n))
+        e = c[0].astype(np.int64) + c[1]
+        for k in range(M):
+            lo, hi = r["slot_off"][k], r["slot_off"][k + 1]
+            for rho in range(R):
+                seg = r["pos_item"][r["llm_off"][k][rho]:r["llm_off"][k][rho + 1]]
+                assert list(seg) == sorted(np.nonzero(a == k * R + rho)[0])
+            tot = int(e[r["pos_item"][lo:hi]].sum())
+            for g in range(1, G):
+                b = r["enc_off"][k][g]
+                pre = int(e[r["pos_item"][lo:b]].sum())
+                assert pre * G >= g * tot or b == hi
+                if b > lo:
+                    assert int(e[r["pos_item"][lo:b - 1]].sum()) * G < g * tot
+            assert int(r["enc_load"][k].sum()) == tot
