@@ -360,6 +360,39 @@ dflop_status dflop_exact_cmax(const uint32_t* cost_ticks, uint32_t n, const dflo
                               const uint32_t* init_assign, void* ws, size_t* ws_bytes, dflop_exact_result* out,
                               uint32_t* assign, dflop_stream_t stream);
 
+/* ---------------------------------------------------------------- N4(a) microbatch order
+ * The 1F1B makespan of a replica depends on the order of its microbatch slots (R11).  For
+ * one assignment (e.g. the search's winner) every LLM replica rho (buckets k * L_dp + rho,
+ * slot k by default, R10) gets an improved slot order: the best of four start orders
+ * (identity, W = max(E, L) ascending, descending, valley), then best-improvement pairwise
+ * slot swaps (every pair when N_mb <= 128, else pairs at distance <= 16), lexicographic
+ * (makespan, a, b), at most `rounds` rounds (R35).
+ *   cost_ticks device u32 [4][n]; assign device u32 [n] (bucket per sample, < m).
+ *   order_out  device u32 [L_dp][N_mb]: the bucket run in slot k of replica rho.
+ *   T_out      host u64 [L_dp]: the replicas' 1F1B makespans (the plan's T = their max).
+ * Synchronous.  Errors: INVALID_ARGUMENT (plan, bucket >= m), UNSUPPORTED (shared memory),
+ * WORKSPACE_TOO_SMALL, CUDA. */
+dflop_status dflop_order_search(const uint32_t* cost_ticks, uint32_t n, const dflop_plan* plan,
+                                const uint32_t* assign, uint32_t rounds, void* ws, size_t* ws_bytes,
+                                uint32_t* order_out, uint64_t* T_out, dflop_stream_t stream);
+
+/* ---------------------------------------------------------------- N4(b) routing plan
+ * The inter-model communicator's plan for E_dp != L_dp: for microbatch slot k the
+ * LLM data groups rho run buckets k * L_dp + rho (R10); the slot's samples, listed in
+ * (rho, sample index) order, are split into E_dp contiguous encoder ranges balanced by the
+ * encoder cost e = ef + eb (range g starts at the first position whose preceding cost
+ * reaches g / E_dp of the slot's total, R36).  Forward: encoder range g is gathered and
+ * scattered over the LLM ranges it overlaps; backward: the reverse.
+ *   cost_ticks device u32 [4][n]; assign device u32 [n] (bucket per sample, < m).
+ *   pos_item   device u32 [n]: the sample at each position (slot-major).
+ *   slot_off   device u32 [N_mb + 1]; enc_off device u32 [N_mb][E_dp + 1]; llm_off device
+ *              u32 [N_mb][L_dp + 1] (absolute positions); enc_load device u64 [N_mb][E_dp]
+ *              or NULL (encoder cost per range).
+ * Synchronous.  Errors: INVALID_ARGUMENT (plan, bucket >= m), WORKSPACE_TOO_SMALL, CUDA. */
+dflop_status dflop_route_plan(const uint32_t* cost_ticks, uint32_t n, const dflop_plan* plan, const uint32_t* assign,
+                              void* ws, size_t* ws_bytes, uint32_t* pos_item, uint32_t* slot_off, uint32_t* enc_off,
+                              uint32_t* llm_off, uint64_t* enc_load, dflop_stream_t stream);
+
 /* ---------------------------------------------------------------- N2 search over a sample
  * Eq. (1): theta* = argmin_theta (1/|D|) sum_{d in D} T(d; theta) over a sample
  * of D global batches, each balanced and scored on the device exactly as in

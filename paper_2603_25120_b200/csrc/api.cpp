@@ -875,6 +875,56 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
 
 }  // namespace dflop
 
+extern "C" dflop_status dflop_route_plan(const uint32_t* cost_ticks, uint32_t n, const dflop_plan* plan,
+                                         const uint32_t* assign, void* ws, size_t* ws_bytes, uint32_t* pos_item,
+                                         uint32_t* slot_off, uint32_t* enc_off, uint32_t* llm_off, uint64_t* enc_load,
+                                         dflop_stream_t stream) {
+    g_err.clear();
+    dflop_status st = validate_plan(plan);
+    if (st != DFLOP_OK) return st;
+    if ((uint64_t)plan->n_mb * plan->l_dp > 65535) return invalid("m = N_mb * L_dp must be <= 65535");
+    if (n > 0 && (!cost_ticks || !assign)) return invalid("cost_ticks / assign are NULL");
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    const size_t need = route_ws_bytes(n, plan);
+    if (!ws) {
+        *ws_bytes = need;
+        return DFLOP_OK;
+    }
+    if (*ws_bytes < need) {
+        set_error("workspace %zu B < required %zu B", *ws_bytes, need);
+        return DFLOP_ERR_WORKSPACE_TOO_SMALL;
+    }
+    if ((uintptr_t)ws % 256) return invalid("workspace must be 256-byte aligned");
+    if (!slot_off || !enc_off || !llm_off || (n > 0 && !pos_item))
+        return invalid("pos_item / slot_off / enc_off / llm_off are NULL");
+    return route_launch(cost_ticks, n, plan, assign, ws, pos_item, slot_off, enc_off, llm_off, enc_load,
+                        (cudaStream_t)stream);
+}
+
+extern "C" dflop_status dflop_order_search(const uint32_t* cost_ticks, uint32_t n, const dflop_plan* plan,
+                                           const uint32_t* assign, uint32_t rounds, void* ws, size_t* ws_bytes,
+                                           uint32_t* order_out, uint64_t* T_out, dflop_stream_t stream) {
+    g_err.clear();
+    dflop_status st = validate_plan(plan);
+    if (st != DFLOP_OK) return st;
+    if (plan->e_pp + plan->l_pp > 32) return invalid("S = E_pp + L_pp must be <= 32");
+    if (plan->n_mb > 65535) return invalid("N_mb must be <= 65535");
+    if (n > 0 && (!cost_ticks || !assign)) return invalid("cost_ticks / assign are NULL");
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    const size_t need = order_ws_bytes(plan);
+    if (!ws) {
+        *ws_bytes = need;
+        return DFLOP_OK;
+    }
+    if (*ws_bytes < need) {
+        set_error("workspace %zu B < required %zu B", *ws_bytes, need);
+        return DFLOP_ERR_WORKSPACE_TOO_SMALL;
+    }
+    if ((uintptr_t)ws % 256) return invalid("workspace must be 256-byte aligned");
+    if (!order_out || !T_out) return invalid("order_out / T_out are NULL");
+    return order_launch(cost_ticks, n, plan, assign, rounds, ws, order_out, T_out, (cudaStream_t)stream);
+}
+
 extern "C" dflop_status dflop_exact_cmax(const uint32_t* cost_ticks, uint32_t n, const dflop_plan* plan,
                                          uint64_t node_budget, const uint32_t* init_assign, void* ws, size_t* ws_bytes,
                                          dflop_exact_result* out, uint32_t* assign, dflop_stream_t stream) {

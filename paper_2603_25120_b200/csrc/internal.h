@@ -114,6 +114,17 @@ __global__ void k_prep_keys(const uint32_t* __restrict__ cost, uint32_t n, size_
 __global__ void k_rank_sort(const u64* __restrict__ keys, uint32_t n, uint32_t* order, uint32_t* item_pos);
 #endif
 
+// ---------------------------------------------------------------- N4(b) routing plan (route.cu)
+size_t route_ws_bytes(uint32_t n, const dflop_plan* p);
+dflop_status route_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p, const uint32_t* assign, void* ws,
+                          uint32_t* pos_item, uint32_t* slot_off, uint32_t* enc_off, uint32_t* llm_off,
+                          uint64_t* enc_load, cudaStream_t s);
+
+// ---------------------------------------------------------------- N4(a) order search (order.cu)
+size_t order_ws_bytes(const dflop_plan* p);
+dflop_status order_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p, const uint32_t* assign,
+                          uint32_t rounds, void* ws, uint32_t* order_out, uint64_t* T_host, cudaStream_t s);
+
 // ---------------------------------------------------------------- N3 exact C_max (exact.cu)
 size_t exact_ws_bytes(uint32_t n, uint32_t m, const dflop_plan* p);
 dflop_status exact_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p, uint64_t node_budget,

@@ -26,7 +26,8 @@ STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE", 3: "OVERFLOW", 4: "INFEASI
 EXPORTS = ["dflop_abi_version", "dflop_last_error", "dflop_release_caches", "dflop_predict_costs",
            "dflop_balance_microbatches", "dflop_simulate_1f1b", "dflop_index_groups", "dflop_search_plans",
            "dflop_get_unique_id", "dflop_comm_init", "dflop_comm_destroy", "dflop_profile_enable",
-           "dflop_profile_read", "dflop_search_plans_batches", "dflop_exact_cmax"]
+           "dflop_profile_read", "dflop_search_plans_batches", "dflop_exact_cmax", "dflop_order_search",
+           "dflop_route_plan"]
 
 
 class DflopError(RuntimeError):
@@ -414,6 +415,51 @@ def exact_cmax(cost_ticks, plan: Dict, node_budget: int = 10 ** 9, init_assign=N
     r["searched"] = bool(r["searched"])
     r["assign"] = assign[:n]
     return r
+
+
+def order_search(cost_ticks, plan: Dict, assign, rounds: int = 64, ws: Optional[Workspace] = None,
+                 stream=None) -> Dict:
+    """N4(a): per replica the improved slot order (bucket per slot) and its 1F1B makespan."""
+    import torch
+    n = cost_ticks.shape[1]
+    dev = cost_ticks.device
+    ps = plan_struct(plan)
+    L = lib()
+    need = C.c_size_t(0)
+    _check(L.dflop_order_search(_ptr(cost_ticks), n, C.byref(ps), _ptr(assign), rounds, None, C.byref(need), None,
+                                None, None))
+    wsb = (ws or _default_ws).get(need.value, dev)
+    have = C.c_size_t(wsb.numel())
+    M, rep = int(plan["n_mb"]), int(plan["l_dp"])
+    order = torch.empty(rep * M, dtype=torch.int32, device=dev)
+    T = np.zeros(rep, np.uint64)
+    _check(L.dflop_order_search(_ptr(cost_ticks), n, C.byref(ps), _ptr(assign), rounds, _ptr(wsb), C.byref(have),
+                                _ptr(order), T.ctypes.data_as(C.c_void_p), _stream(stream)))
+    return dict(order=order.view(rep, M), T=T, makespan=int(T.max()) if rep else 0)
+
+
+def route_plan(cost_ticks, plan: Dict, assign, ws: Optional[Workspace] = None, stream=None) -> Dict:
+    """N4(b): the inter-model communicator's routing plan (device tensors)."""
+    import torch
+    n = cost_ticks.shape[1]
+    dev = cost_ticks.device
+    ps = plan_struct(plan)
+    L = lib()
+    need = C.c_size_t(0)
+    _check(L.dflop_route_plan(_ptr(cost_ticks), n, C.byref(ps), _ptr(assign), None, C.byref(need), None, None, None,
+                              None, None, None))
+    wsb = (ws or _default_ws).get(need.value, dev)
+    have = C.c_size_t(wsb.numel())
+    M, R, G = int(plan["n_mb"]), int(plan["l_dp"]), int(plan["e_dp"])
+    pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    so = torch.empty(M + 1, dtype=torch.int32, device=dev)
+    eo = torch.empty(M * (G + 1), dtype=torch.int32, device=dev)
+    lo = torch.empty(M * (R + 1), dtype=torch.int32, device=dev)
+    el = torch.empty(M * G, dtype=torch.int64, device=dev)
+    _check(L.dflop_route_plan(_ptr(cost_ticks), n, C.byref(ps), _ptr(assign), _ptr(wsb), C.byref(have), _ptr(pos),
+                              _ptr(so), _ptr(eo), _ptr(lo), _ptr(el), _stream(stream)))
+    return dict(pos_item=pos[:n], slot_off=so, enc_off=eo.view(M, G + 1), llm_off=lo.view(M, R + 1),
+                enc_load=el.view(M, G))
 
 
 def search_plans_batches(model: Dict, tiles, frames, text, batch_offsets: Sequence[int], K: int, R: int, G: int,
