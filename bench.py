@@ -303,6 +303,11 @@ def main():
             roofline["traffic"] = tr["dram_bytes_per_candidate"] * (e - b)
             roofline["traffic_unit"] = "B"
             roofline["traffic_source"] = tr["source"]
+            # the same capture's achieved instruction issue (smsp__issue_active, % of peak):
+            # the issue roofline the kernel runs at, beside the algorithmic-op fraction above
+            if "ncu_issue_active" in tr:
+                roofline["ncu_issue_active"] = tr["ncu_issue_active"]
+                roofline["ncu_threads_per_warp_instruction"] = tr.get("ncu_threads_per_warp_instruction")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
