@@ -334,6 +334,61 @@ DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t es, 
     }
 }
 
+// Two consecutive samples A, B of the (perturbed) order in one step of the packed variant
+// with 8 buckets per lane -- exactly the sequential decisions: B's argmin is computed on the
+// loads before A's update together with its runner-up; A's update only raises bucket a*, so
+// if B's best b1 is not a* it stays B's argmin (ties: the packed keys carry the index), and
+// if b1 = a*, B's argmin is the smaller of the runner-up and a*'s key after A's update
+// (computed by a*'s owner lane and broadcast).  Halves the dependent reduction chains.
+template <int GL>
+DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* apos, uint32_t pa, uint32_t pb,
+                             const ItemRec<uint32_t>& ia, const ItemRec<uint32_t>& ib, uint32_t use, uint32_t jmask,
+                             uint32_t gl, uint32_t lane) {
+    const uint32_t esa = ia.e & use, lsa = ia.l & use, esb = ib.e & use, lsb = ib.l & use;
+    uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+#pragma unroll
+    for (uint32_t k = 0; k < 8; k += 2) {
+        const Pair2<uint32_t> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
+        a0 = min(a0, max(x.a + esa, x.b + lsa));
+        a1 = min(a1, max(y.a + esa, y.b + lsa));
+        const uint32_t vx = max(x.a + esb, x.b + lsb), vy = max(y.a + esb, y.b + lsb);
+        m2 = min(m2, max(m1, vx));
+        m1 = min(m1, vx);
+        m2 = min(m2, max(m1, vy));
+        m1 = min(m1, vy);
+    }
+    uint32_t ba = min(a0, a1);
+#pragma unroll
+    for (int off = GL / 2; off > 0; off >>= 1) {
+        ba = min(ba, __shfl_xor_sync(FULL, ba, off));
+        const uint32_t o1 = __shfl_xor_sync(FULL, m1, off), o2 = __shfl_xor_sync(FULL, m2, off);
+        m2 = min(max(m1, o1), min(m2, o2));  // second smallest of the two sorted pairs
+        m1 = min(m1, o1);
+    }
+    const uint32_t ja = ba & jmask;
+    const bool own_a = (ja & (GL - 1)) == gl;
+    Pair2<uint32_t> ela{0, 0};
+    uint32_t alt = 0xFFFFFFFFu;
+    if (own_a) {
+        ela = EL[ja];
+        alt = min(m2, max(ela.a + ia.e + esb, ela.b + ia.l + lsb));  // a* after A, probed by B
+    }
+    alt = __shfl_sync(FULL, alt, (lane & ~(uint32_t)(GL - 1)) | (ja & (GL - 1)));
+    const uint32_t jb = (((m1 & jmask) != ja) ? m1 : alt) & jmask;
+    if (own_a) {
+        EL[ja] = Pair2<uint32_t>{ela.a + ia.e, ela.b + ia.l};
+        Pair2<uint32_t> fl = FL[ja];
+        FL[ja] = Pair2<uint32_t>{fl.a + ia.ef, fl.b + ia.lf};
+        apos[pa] = (uint8_t)ja;
+    }
+    if ((jb & (GL - 1)) == gl) {  // after A's update in program order when jb = ja (same lane)
+        const Pair2<uint32_t> el = EL[jb], fl = FL[jb];
+        EL[jb] = Pair2<uint32_t>{el.a + ib.e, el.b + ib.l};
+        FL[jb] = Pair2<uint32_t>{fl.a + ib.ef, fl.b + ib.lf};
+        apos[pb] = (uint8_t)jb;
+    }
+}
+
 // ---------------------------------------------------------------- LPT pass (R12)
 // c == 0: argmin of the current max(E_j, L_j) (the paper's rule); c >= 1: argmin of the
 // resulting max(E_j + e_i, L_j + l_i); lowest j on ties.
@@ -354,7 +409,20 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
         const uint32_t start = (g0 + gg) * G;
         const uint32_t ng = min(G, n - start);
         const uint64_t perm = nc ? __shfl_sync(FULL, preg, mycg * W + gg) : 0xFEDCBA9876543210ull;
-        for (uint32_t t = 0; t < ng; ++t) {
+        uint32_t t = 0;
+#ifndef DFLOP_NO_LPT_PAIRS
+        if constexpr (PK) {
+            if (m == 8 * GL) {  // two samples per step (see lpt_pair_step)
+                for (; t + 1 < ng; t += 2) {
+                    const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
+                    const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
+                    lpt_pair_step<GL>(reinterpret_cast<Pair2<uint32_t>*>(EL), reinterpret_cast<Pair2<uint32_t>*>(FL),
+                                      apos, pa, pb, T.item(pa), T.item(pb), (uint32_t)use, jmask, gl, lane);
+                }
+            }
+        }
+#endif
+        for (; t < ng; ++t) {
             const uint32_t pos = start + (uint32_t)((perm >> (4 * t)) & 15ull);
             const ItemRec<A> it = T.item(pos);
             uint32_t bj;
