@@ -87,7 +87,7 @@ __global__ void k_rank_sort(const u64* __restrict__ keys, uint32_t n, uint32_t* 
 
 // Chooses the candidate-kernel variant and writes the per-position records.
 //   u32 when every bucket sum fits (sums of all e_i, l_i below 2^32 - 1);
-//   packed u32 when m <= 255 (one-byte assignment) and every LPT bucket load stays below
+//   packed u32 when every LPT bucket load stays below
 //   2^(32 - s), s = bits of m - 1:
 //   a probe's winner has W <= min_j W_j + max(e, l) <= (sum_e + sum_l)/m + max key, every
 //   probe adds at most one more max key, and refinement never raises the maximum (O6).
@@ -98,7 +98,7 @@ __global__ void k_build_items(const uint32_t* __restrict__ cost, uint32_t n, siz
     uint32_t sh = 0;
     while ((1u << sh) < m) ++sh;
     const u64 bound = (hdr->sum_e + hdr->sum_l + m - 1) / m + 2 * hdr->max_key;
-    const bool packed = allow_pack && fits && m <= 255 && sh < 32 && bound < (1ull << (32 - sh));
+    const bool packed = allow_pack && fits && sh < 32 && bound < (1ull << (32 - sh));
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         hdr->variant = packed ? 0u : (fits ? 1u : 2u);
         hdr->shift = sh;

@@ -396,7 +396,7 @@ template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
                         Pair2<A>* FL, uint8_t* apos, uint32_t gl) {
     const uint32_t n = p.n, m = p.m, G = p.G;
-    const bool wide = PK ? false : p.wide != 0;  // the packed variant requires m <= 255
+    const bool wide = p.wide != 0;  // u16 assignment when m > 255
     const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
     const uint32_t jmask = (1u << sh) - 1u;
     const uint32_t nc = (G - 1 + 3) / 4;  // Philox calls per group
@@ -412,7 +412,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
         uint32_t t = 0;
 #ifndef DFLOP_NO_LPT_PAIRS
         if constexpr (PK) {
-            if (m == 8 * GL) {  // two samples per step (see lpt_pair_step)
+            if (m == 8 * GL && !wide) {  // two samples per step (see lpt_pair_step; u8 assignment)
                 for (; t + 1 < ng; t += 2) {
                     const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
@@ -506,7 +506,7 @@ template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
                       uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, bool apply, PhaseTimer& ph) {
     const uint32_t m = p.m, cap = p.cap;
-    const bool wide = PK ? false : p.wide != 0;  // the packed variant requires m <= 255
+    const bool wide = p.wide != 0;  // u16 assignment when m > 255
     // cnt[m] members per bucket, off[m + 1] list starts: in shared memory (m <= 256), else
     // in front of the slot's global lists; then the shared-memory copies of the first cap
     // members of j* (ls) and j' (lp)
