@@ -316,3 +316,50 @@ def test_search_infeasible(D, presets):
         D.search_plans(p.model, dt, df, dx, K=4, R=1, G=8, seed=(1, 1), cluster=p.cluster, mem=mem, gbs=p.gbs,
                        top_p=2)
     assert e.value.code == 4
+
+
+def test_config3_full_family_per_gpu_sampled(D, O, presets):
+    """Config 3 at its full per-GPU family (K = 65,536, weak scaling): winner re-derived from
+    the per-candidate array, sampled candidates recomputed by the oracle."""
+    p = presets[3]
+    (t, f, x), (dt, df, dx) = feats(p, 1)
+    _, ticks = D.predict_costs(p.model, p.plan, dt, df, dx, want_f32=False)
+    r = D.balance_microbatches(ticks, p.plan, p.K, p.R, p.G, p.seed(1), per_candidate=True)
+    best = D.cand_result(r["best"])
+    cT, cC = host_u64(r["cand_T"]), host_u64(r["cand_cmax"])
+    c_star = int(np.lexsort((np.arange(p.K), cT))[0])
+    assert best["cand"] == c_star and best["makespan"] == cT[c_star]
+    q = host_u32(ticks)
+    pi = O.base_order(q)
+    rng = np.random.default_rng(5)
+    for c in sorted(set([0, 1, 2, p.K - 1, c_star] + rng.integers(0, p.K, 40).tolist())):
+        a, T, cm = O.run_candidate(q, p.plan, p.K, p.R, p.G, p.seed(1), c, order=pi)
+        assert (T, cm) == (int(cT[c]), int(cC[c])), c
+        if c == c_star:
+            assert (host_u32(r["assign"]) == a).all()
+
+
+def test_config4_full_search_plans_rebalanced(D, O, presets):
+    """Config 4 at full size (P = 64 plans x K = 4,096): the per-plan T_B of Stage B for the
+    Stage-A leader, the winner and the last plan re-derived by the oracle's balance of the
+    same costs over the whole family."""
+    p = presets[4]
+    (t, f, x), (dt, df, dx) = feats(p, 0)
+    res = D.search_plans_batches(p.model, dt, df, dx, [0, p.n], K=p.K, R=p.R, G=p.G, seed=p.seed(0),
+                                 cluster=p.cluster, mem=p.mem(), gbs=p.gbs, top_p=p.top_p)
+    mb, ms = O.batch_means(p.model, t, f, x)
+    T_A, cfgs = O.stage_a_all(p.model, p.mem(), p.cluster["n_gpus"], p.cluster["gpus_per_node"], p.gbs, mb, ms)
+    top = O.stage_a_top(T_A, p.top_p)
+    obj = res["plan_objective"]
+    win = res["stage_a_rank"]
+    assert int(obj[win]) == res["makespan"] == min(int(v) for v in obj)
+    for rank in sorted({0, win, len(top) - 1}):
+        e, i = O.pair_to_config(cfgs, p.gbs, top[rank])
+        c = cfgs[e]
+        pl = dict(e_tp=int(c[0]), e_pp=int(c[1]), e_dp=int(c[2]), l_tp=int(c[3]), l_pp=int(c[4]), l_dp=int(c[5]),
+                  n_mb=i)
+        _, ticks = D.predict_costs(p.model, pl, dt, df, dx, want_f32=False)
+        o = O.balance_threaded(host_u32(ticks), pl, p.K, p.R, p.G, p.seed(0), per_candidate=False)
+        assert int(obj[rank]) == o["T"], rank
+        if rank == win:
+            assert res["cand"] == o["c"] and res["cmax"] == o["cmax"]
