@@ -25,7 +25,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("k, batches", [(2, 0), (3, 0), (5, 0), (2, 3)])
+@pytest.mark.parametrize("k, batches", [(2, 0), (3, 0), (5, 0), (2, 3), (4, 0), (4, 2)])
 def test_sharded_search_equals_single_gpu(k, batches):
     n = torch.cuda.device_count()
     if n < 2:

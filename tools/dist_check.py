@@ -31,16 +31,17 @@ torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 p = synth.presets()[a.config]
 comm = D.Comm(rank, world, local)
+search_kw = dict(plan=p.plan) if p.plan is not None else dict(cluster=p.cluster, mem=p.mem(), gbs=p.gbs, top_p=16)
 if a.batches:
     feats = [p.features(b) for b in range(a.batches)]
     offs = np.concatenate([[0], np.cumsum([len(fb[0]) for fb in feats])])
     t, f, x = (torch.from_numpy(np.concatenate([fb[i] for fb in feats]).astype(np.uint32).view(np.int32)).cuda()
                for i in range(3))
     run = lambda cm: D.search_plans_batches(p.model, t, f, x, offs, K=a.K, R=p.R, G=p.G, seed=p.seed(0),
-                                            plan=p.plan, comm=cm)
+                                            comm=cm, **search_kw)
 else:
     t, f, x = (torch.from_numpy(v.astype(np.uint32).view(np.int32)).cuda() for v in p.features(0))
-    run = lambda cm: D.search_plans(p.model, t, f, x, K=a.K, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan, comm=cm)
+    run = lambda cm: D.search_plans(p.model, t, f, x, K=a.K, R=p.R, G=p.G, seed=p.seed(0), comm=cm, **search_kw)
 res = run(comm)
 assign = res["assign"].cpu().numpy()
 ok = True
@@ -49,6 +50,7 @@ if rank == 0:
     ok = (res["makespan"], res["cand"], res["cmax"]) == (ref["makespan"], ref["cand"], ref["cmax"])
     ok = ok and bool((assign == ref["assign"].cpu().numpy()).all())
     ok = ok and res["owner_rank"] == sharding.owner_of(a.K, res["cand"], world)
+    ok = ok and res["plan"] == ref["plan"] and res["stage_a_rank"] == ref["stage_a_rank"]
     if a.batches:
         ok = ok and [b["makespan"] for b in res["batches"]] == [b["makespan"] for b in ref["batches"]]
 # every rank must hold the same winner and assignment
