@@ -363,3 +363,13 @@ def test_config4_full_search_plans_rebalanced(D, O, presets):
         assert int(obj[rank]) == o["T"], rank
         if rank == win:
             assert res["cand"] == o["c"] and res["cmax"] == o["cmax"]
+
+
+def test_global_item_table_path(D, O, presets):
+    """n large enough that the per-CTA item table does not fit in shared memory (the kernel
+    reads the records from global memory): parity on a window of candidates."""
+    p = presets[5]
+    t, f, x = (np.tile(a, 5)[:20000] for a in p.features(4))
+    _, q, st, _ = O.predict(p.model, p.plan, t, f, x)
+    assert st == 0
+    check_balance(D, O, q, p.plan, 4096, 4, p.G, p.seed(4), 100, 148)
