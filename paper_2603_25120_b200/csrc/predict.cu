@@ -23,7 +23,7 @@ struct PredictKnots {
     float x[DFLOP_MAX_X];
     float inv[DFLOP_MAX_X];  // 1 / (x[k+1] - x[k]) (from double)
     int n_x;
-    int pad;
+    int e0;                  // knots are exactly 2^(e0 + k): k from the float exponent; else -1000
 };
 struct PredictGrids {
     PredictKnots e, att, lin;
@@ -56,9 +56,13 @@ DFLOP_DEV float interp_row(const PredictKnots& g, const float* v, float x) {
     if (n == 1) return v[0];
     const float xh = fminf(fmaxf(x, g.x[0]), g.x[n - 1]);
     int k = 0;
+    if (g.e0 > -1000) {  // power-of-two knots: floor(log2 xh) - e0, the same k as the search
+        k = min((int)(__float_as_uint(xh) >> 23) - 127 - g.e0, n - 2);
+    } else {
 #pragma unroll
-    for (int step = DFLOP_MAX_X / 2; step > 0; step >>= 1)
-        if (k + step <= n - 2 && g.x[k + step] <= xh) k += step;
+        for (int step = DFLOP_MAX_X / 2; step > 0; step >>= 1)
+            if (k + step <= n - 2 && g.x[k + step] <= xh) k += step;
+    }
     const float w = (xh - g.x[k]) * g.inv[k];
     return (1.0f - w) * v[k] + w * v[k + 1];
 }
@@ -144,7 +148,15 @@ __global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaun
 
 static void to_knots(const dflop_grid& s, PredictKnots& d) {
     d.n_x = (int)s.n_x;
-    d.pad = 0;
+    // knots x_k = 2^(e0 + k) exactly, with 2^e0 >= 1 (every float in range is normal)
+    d.e0 = -1000;
+    if (s.n_x >= 2 && s.x[0] >= 1.0) {
+        int e0 = 0;
+        const double f = std::frexp(s.x[0], &e0);  // x0 = f * 2^e0, f in [0.5, 1)
+        bool pow2 = f == 0.5;
+        for (uint32_t k = 0; pow2 && k < s.n_x; ++k) pow2 = s.x[k] == std::ldexp(1.0, e0 - 1 + (int)k);
+        if (pow2 && e0 - 1 + (int)s.n_x < 127) d.e0 = e0 - 1;
+    }
     for (int k = 0; k < DFLOP_MAX_X; ++k) {
         d.x[k] = k < (int)s.n_x ? (float)s.x[k] : 0.0f;
         d.inv[k] = k + 1 < (int)s.n_x ? (float)(1.0 / (s.x[k + 1] - s.x[k])) : 0.0f;
