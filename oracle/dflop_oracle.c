@@ -377,13 +377,16 @@ static int score_partition(const bucket_sums* bk, const orc_plan* p, uint64_t* T
     return st;
 }
 
+static uint64_t best_start_order(const bucket_sums* bk, const orc_plan* p, uint32_t rho, uint64_t* F, uint64_t* B,
+                                 uint32_t* ord);
+
 int orc_run_candidate(const uint32_t* q, uint32_t n, const orc_plan* p, const orc_bparams* bp,
                       const uint32_t* pi, uint32_t c, uint32_t* assign_out, uint64_t* T, uint64_t* cmax) {
     uint32_t m = p->n_mb * p->l_dp;
     bucket_sums* bk = (bucket_sums*)calloc(m, sizeof(bucket_sums));
     uint32_t* a = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
     uint32_t* order = (uint32_t*)malloc(sizeof(uint32_t) * (n + 1)); /* +1: refinement partner list */
-    if (bp->mode == 1) {
+    if (bp->mode & ORC_MODE_EXHAUSTIVE) {
         /* EXHAUSTIVE: candidate c is the base-m number a_{n-1} ... a_1 a_0 (requires m^n <= K). */
         uint64_t x = c;
         for (uint32_t i = 0; i < n; i++) { a[i] = (uint32_t)(x % m); x /= m; add_item(&bk[a[i]], q, n, i); }
@@ -457,6 +460,18 @@ int orc_run_candidate(const uint32_t* q, uint32_t n, const orc_plan* p, const or
         }
     }
     int st = score_partition(bk, p, T, cmax);
+    if (st == ORC_OK && (bp->mode & ORC_MODE_ORDER4)) {
+        /* N4(a) per candidate: every replica runs its best start order; T = the max over
+         * replicas of that minimum (R37) */
+        uint32_t S = p->e_pp + p->l_pp, M = p->n_mb;
+        uint64_t* F = (uint64_t*)malloc(sizeof(uint64_t) * S * M);
+        uint64_t* B = (uint64_t*)malloc(sizeof(uint64_t) * S * M);
+        uint32_t* ord = (uint32_t*)malloc(sizeof(uint32_t) * M);
+        uint64_t Tb = 0;
+        for (uint32_t rho = 0; rho < p->l_dp; rho++) Tb = max64(Tb, best_start_order(bk, p, rho, F, B, ord));
+        *T = Tb;
+        free(F); free(B); free(ord);
+    }
     if (assign_out) memcpy(assign_out, a, sizeof(uint32_t) * n);
     free(bk); free(a); free(order);
     return st;
@@ -579,6 +594,52 @@ static uint64_t order_makespan(const bucket_sums* bk, const orc_plan* p, uint32_
     return T;
 }
 
+/* The four start orders of replica rho (N4(a), R35): 0 slot order, 1 ascending W_j =
+ * max(E_j, L_j), 2 descending W (ties by slot), 3 valley; returns the least makespan (ties:
+ * lowest order index) and that order in ord[M]. */
+static uint64_t best_start_order(const bucket_sums* bk, const orc_plan* p, uint32_t rho, uint64_t* F, uint64_t* B,
+                                 uint32_t* ord) {
+    uint32_t M = p->n_mb;
+    uint32_t* cand = (uint32_t*)malloc(sizeof(uint32_t) * M);
+    uint32_t* asc = (uint32_t*)malloc(sizeof(uint32_t) * M);
+    uint64_t* W = (uint64_t*)malloc(sizeof(uint64_t) * M);
+    for (uint32_t k = 0; k < M; k++) {
+        const bucket_sums* b = &bk[k * p->l_dp + rho];
+        W[k] = max64(bE(b), bL(b));
+        asc[k] = k;
+    }
+    for (uint32_t a = 1; a < M; a++) { /* stable insertion sort by W ascending */
+        uint32_t x = asc[a], b = a;
+        while (b > 0 && W[asc[b - 1]] > W[x]) { asc[b] = asc[b - 1]; b--; }
+        asc[b] = x;
+    }
+    uint64_t bestT = 0;
+    for (uint32_t o = 0; o < 4; o++) {
+        if (o == 0) for (uint32_t k = 0; k < M; k++) cand[k] = k;
+        if (o == 1) for (uint32_t k = 0; k < M; k++) cand[k] = asc[k];
+        if (o == 2) { /* descending W, ties by slot ascending */
+            uint32_t k = 0;
+            for (uint32_t e = M; e > 0;) {
+                uint32_t s0 = e - 1;
+                while (s0 > 0 && W[asc[s0 - 1]] == W[asc[e - 1]]) s0--;
+                for (uint32_t t = s0; t < e; t++) cand[k++] = asc[t];
+                e = s0;
+            }
+        }
+        if (o == 3) { /* valley */
+            uint32_t lo = 0, hi = M - 1;
+            for (uint32_t t = 0; t < M; t++) {
+                if (t % 2 == 0) cand[lo++] = asc[t];
+                else cand[hi--] = asc[t];
+            }
+        }
+        uint64_t T = order_makespan(bk, p, rho, cand, F, B);
+        if (o == 0 || T < bestT) { bestT = T; memcpy(ord, cand, sizeof(uint32_t) * M); }
+    }
+    free(cand); free(asc); free(W);
+    return bestT;
+}
+
 int orc_order_search(const uint32_t* q, uint32_t n, const orc_plan* p, const uint32_t* assign, uint32_t rounds,
                      uint32_t* order_out, uint64_t* T_out) {
     uint32_t m = p->n_mb * p->l_dp, M = p->n_mb, S = p->e_pp + p->l_pp;
@@ -589,45 +650,9 @@ int orc_order_search(const uint32_t* q, uint32_t n, const orc_plan* p, const uin
     }
     uint64_t* F = (uint64_t*)malloc(sizeof(uint64_t) * S * M);
     uint64_t* B = (uint64_t*)malloc(sizeof(uint64_t) * S * M);
-    uint32_t* cand = (uint32_t*)malloc(sizeof(uint32_t) * M);
     uint32_t* ord = (uint32_t*)malloc(sizeof(uint32_t) * M);
-    uint64_t* W = (uint64_t*)malloc(sizeof(uint64_t) * M);
-    uint32_t* asc = (uint32_t*)malloc(sizeof(uint32_t) * M);
     for (uint32_t rho = 0; rho < p->l_dp; rho++) {
-        for (uint32_t k = 0; k < M; k++) {
-            const bucket_sums* b = &bk[k * p->l_dp + rho];
-            W[k] = max64(bE(b), bL(b));
-            asc[k] = k;
-        }
-        /* stable insertion sort of the slots by W ascending */
-        for (uint32_t a = 1; a < M; a++) {
-            uint32_t x = asc[a], b = a;
-            while (b > 0 && W[asc[b - 1]] > W[x]) { asc[b] = asc[b - 1]; b--; }
-            asc[b] = x;
-        }
-        uint64_t bestT = 0;
-        for (uint32_t o = 0; o < 4; o++) {
-            if (o == 0) for (uint32_t k = 0; k < M; k++) cand[k] = k;
-            if (o == 1) for (uint32_t k = 0; k < M; k++) cand[k] = asc[k];
-            if (o == 2) { /* descending W, ties by slot ascending */
-                uint32_t k = 0;
-                for (uint32_t e = M; e > 0;) {
-                    uint32_t s0 = e - 1; /* run of equal W ending at e-1 in asc */
-                    while (s0 > 0 && W[asc[s0 - 1]] == W[asc[e - 1]]) s0--;
-                    for (uint32_t t = s0; t < e; t++) cand[k++] = asc[t];
-                    e = s0;
-                }
-            }
-            if (o == 3) { /* valley */
-                uint32_t lo = 0, hi = M - 1;
-                for (uint32_t t = 0; t < M; t++) {
-                    if (t % 2 == 0) cand[lo++] = asc[t];
-                    else cand[hi--] = asc[t];
-                }
-            }
-            uint64_t T = order_makespan(bk, p, rho, cand, F, B);
-            if (o == 0 || T < bestT) { bestT = T; memcpy(ord, cand, sizeof(uint32_t) * M); }
-        }
+        uint64_t bestT = best_start_order(bk, p, rho, F, B, ord);
         for (uint32_t r = 0; r < rounds; r++) {
             uint64_t rT = 0;
             uint32_t ra = 0, rb = 0;
@@ -647,7 +672,7 @@ int orc_order_search(const uint32_t* q, uint32_t n, const orc_plan* p, const uin
         for (uint32_t k = 0; k < M; k++) order_out[rho * M + k] = ord[k] * p->l_dp + rho;
         T_out[rho] = bestT;
     }
-    free(bk); free(F); free(B); free(cand); free(ord); free(W); free(asc);
+    free(bk); free(F); free(B); free(ord);
     return ORC_OK;
 }
 

@@ -72,8 +72,11 @@ typedef struct orc_plan {
     uint32_t e_tp, e_pp, e_dp, l_tp, l_pp, l_dp, n_mb;
 } orc_plan;
 
+#define ORC_MODE_EXHAUSTIVE 1u  /* candidate c = base-m digits                          */
+#define ORC_MODE_ORDER4 16u     /* score each replica under its best of the four start
+                                   orders of N4(a) (R37) instead of the slot order       */
 typedef struct orc_bparams {
-    uint32_t mode;       /* 0 = heuristic candidate family, 1 = exhaustive */
+    uint32_t mode;       /* 0 = heuristic candidate family, ORC_MODE_* bits */
     uint32_t K;          /* family size                                   */
     uint32_t R;          /* refinement rounds                             */
     uint32_t G;          /* perturbation group size 1..16                 */

@@ -693,3 +693,18 @@ def test_route_plan_paper_figure_and_invariants(O):
                 if b > lo:
                     assert int(e[r["pos_item"][lo:b - 1]].sum()) * G < g * tot
             assert int(r["enc_load"][k].sum()) == tot
+
+
+def test_order4_mode_per_candidate(O, presets):
+    # R37: with ORDER4 a candidate's T is the max over replicas of the best of the four start
+    # orders -- the rounds = 0 order search of its assignment; never above the slot order
+    for k, pl_over in [(2, None), (3, None), (2, dict(l_dp=2, n_mb=8))]:
+        p = presets[k]
+        pl = dict(p.plan, **pl_over) if pl_over else p.plan
+        _, q, _, _ = O.predict(p.model, pl, *p.features(0))
+        pi = O.base_order(q)
+        for c in (0, 1, 2, 17, 300):
+            a, T0, cm0 = O.run_candidate(q, pl, p.K, p.R, p.G, p.seed(0), c, order=pi)
+            a4, T4, cm4 = O.run_candidate(q, pl, p.K, p.R, p.G, p.seed(0), c, order=pi, mode=16)
+            _, Tr = O.order_search(q, pl, a, rounds=0)
+            assert (a4 == a).all() and cm4 == cm0 and T4 == int(Tr.max()) and T4 <= T0
