@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle baseline budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--order4", action="store_true", help="DFLOP_MODE_ORDER4: per-candidate slot-order choice")
     return ap.parse_args()
 
 
@@ -212,7 +213,7 @@ def main():
     def step(b):
         t, f, x = dfeat[b % n_batches]
         return D.search_plans(p.model, t, f, x, K=K, R=p.R, G=p.G, seed=p.seed(b % n_batches), plan=p.plan,
-                              comm=comm, want_assign=True, ws=ws)
+                              comm=comm, want_assign=True, ws=ws, order4=args.order4)
 
     for i in range(max(3, args.warmup)):
         step(i)
@@ -265,7 +266,7 @@ def main():
             for d_, h_ in zip(dbuf, pinned[i % n_batches]):
                 d_.copy_(h_, non_blocking=True)
             r = D.search_plans(p.model, *dbuf, K=K, R=p.R, G=p.G, seed=p.seed(i % n_batches), plan=p.plan,
-                               comm=comm, want_assign=True, ws=ws)
+                               comm=comm, want_assign=True, ws=ws, order4=args.order4)
             out_host.copy_(r["assign"], non_blocking=True)
             e1.record(stream)
             e1.synchronize()
@@ -313,7 +314,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "K_per_gpu": K // world, "R": p.R,
+        "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "K_per_gpu": K // world, "order4": bool(args.order4), "R": p.R,
                    "G": p.G, "plan": p.plan, "tick_ns": p.model["tick_ns"],
                    "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"candidate-shard x{world}"},
         "p50_plan_latency_ms": p50, "p99_plan_latency_ms": p99,

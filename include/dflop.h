@@ -146,6 +146,12 @@ typedef struct dflop_cluster {
 
 #define DFLOP_MODE_HEURISTIC 0u  /* the seeded LPT + swap-refinement family       */
 #define DFLOP_MODE_EXHAUSTIVE 1u /* candidate c = base-m digits of c (m^n <= K)    */
+/* N4(a) per candidate (R37), OR-ed into dflop_balance_params.mode or
+ * dflop_search_params.mode: every replica of a candidate is scored under its best of the
+ * four start orders of dflop_order_search (slot order, W ascending, W descending, valley);
+ * T = the max over replicas of that minimum.  The winner's slot order is
+ * dflop_order_search(assign, rounds = 0). */
+#define DFLOP_MODE_ORDER4 16u
 
 /* Candidate family.  c = 0: the paper's LPT (current-load rule,
  * P:738); c = 1: resulting-max LPT (R12); c >= 2: Philox-perturbed order, resulting-max

@@ -171,14 +171,14 @@ static dflop_status validate_bparams(const dflop_balance_params* bp, uint32_t n,
     if (bp->struct_size != sizeof(dflop_balance_params))
         return invalid("dflop_balance_params.struct_size=%u, expected %zu", bp->struct_size,
                        sizeof(dflop_balance_params));
-    if (bp->mode > 1) return invalid("mode %u unknown", bp->mode);
+    if (bp->mode & ~(DFLOP_MODE_EXHAUSTIVE | DFLOP_MODE_ORDER4)) return invalid("mode %u unknown", bp->mode);
     if (bp->K == 0 || bp->K > (1u << 24)) return invalid("K=%u outside 1..2^24", bp->K);
     if (bp->cand_begin >= bp->cand_end || bp->cand_end > bp->K)
         return invalid("shard [%u, %u) empty or outside [0, K=%u)", bp->cand_begin, bp->cand_end, bp->K);
     if ((uint64_t)bp->id_base + bp->K > (1u << 24)) return invalid("id_base + K must be <= 2^24 (packed key)");
     if (bp->G < 1 || bp->G > 16) return invalid("G=%u outside 1..16", bp->G);
     if (bp->R > 4096) return invalid("R=%u > 4096", bp->R);
-    if (bp->mode == DFLOP_MODE_EXHAUSTIVE) {
+    if (bp->mode & DFLOP_MODE_EXHAUSTIVE) {
         double cnt = std::pow((double)m, (double)n);
         if (cnt > (double)bp->K) return invalid("EXHAUSTIVE needs m^n = %.0f <= K = %u", cnt, bp->K);
     }
@@ -549,7 +549,7 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
     if (st != DFLOP_OK) return st;
     if (!sp || sp->struct_size != sizeof(dflop_search_params)) return invalid("dflop_search_params struct_size");
     if (!ws_bytes) return invalid("ws_bytes is NULL");
-    if (sp->mode > 1) return invalid("search mode %u unknown", sp->mode);
+    if (sp->mode & ~(1u | DFLOP_MODE_ORDER4)) return invalid("search mode %u unknown", sp->mode);
     if (sp->K == 0 || sp->K > (1u << 24)) return invalid("K=%u outside 1..2^24", sp->K);
     if (sp->G < 1 || sp->G > 16) return invalid("G=%u outside 1..16", sp->G);
     if (sp->R > 4096) return invalid("R=%u > 4096", sp->R);
@@ -572,7 +572,8 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
     text += off[0];
     const int dev = current_device();
     const uint32_t gbs = sp->gbs ? sp->gbs : n_max;
-    const bool alg1 = sp->mode == DFLOP_SEARCH_ALG1;
+    const bool alg1 = (sp->mode & 1u) == DFLOP_SEARCH_ALG1;
+    const uint32_t bmode = DFLOP_MODE_HEURISTIC | (sp->mode & DFLOP_MODE_ORDER4);
     uint32_t P = 1, m_max = 0;
     const ConfigTable* tab = nullptr;
     if (alg1) {
@@ -602,7 +603,7 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
         bal_bytes = balance_bound(n_max, std::max(1u, m_max), std::max(1u, cend - cb), dev);
     } else if (cend > cb) {
         BalancePlan bp0;
-        if ((st = plan_balance(n_max, &sp->fixed_plan, DFLOP_MODE_HEURISTIC, sp->R, sp->G, cend - cb, &bp0)) != DFLOP_OK)
+        if ((st = plan_balance(n_max, &sp->fixed_plan, bmode, sp->R, sp->G, cend - cb, &bp0)) != DFLOP_OK)
             return st;
         bal_bytes = bp0.cfg.total;
     }
@@ -721,7 +722,7 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
                 continue;
             }
             BalancePlan bpn;
-            if ((st = plan_balance(nb, &plans[p], DFLOP_MODE_HEURISTIC, sp->R, sp->G, cend - cb, &bpn)) != DFLOP_OK)
+            if ((st = plan_balance(nb, &plans[p], bmode, sp->R, sp->G, cend - cb, &bpn)) != DFLOP_OK)
                 return st;
             if (bpn.cfg.total > L.bal_bytes) {
                 set_error("internal: balance workspace %zu > bound %zu", bpn.cfg.total, L.bal_bytes);

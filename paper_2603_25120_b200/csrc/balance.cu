@@ -316,8 +316,10 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     cfg.cnt_smem = m <= 256;
     const size_t hdr_u16 = cfg.cnt_smem ? 0 : 2 * (2 * (size_t)m + 1);
     cfg.csr_len = (uint32_t)((hdr_u16 + (size_t)n + (size_t)m * cfg.sigma + 7) & ~(size_t)7);
-    // scratch: [cnt, off,] ls[cap], lp[cap] (u16) -- or the 1F1B rings
-    const uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cfg.cap, (S + 2 * S * sh.D) * 8u));
+    // scratch: [cnt, off,] ls[cap], lp[cap] (u16) -- or the 1F1B rings (and, with ORDER4, the
+    // ascending / descending slot orders, u16)
+    const uint32_t rings = (S + 2 * S * sh.D) * 8u + ((sh.mode & DFLOP_MODE_ORDER4) ? 4u * sh.n_mb : 0u);
+    const uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cfg.cap, rings));
     const size_t smem_max = prop.smem_optin;
     const uint32_t nsm = (uint32_t)prop.sms;
     const uint32_t per_warp = 32u / (uint32_t)gl;  // candidate groups per warp
@@ -352,7 +354,8 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
             return cfg;
         }
         const size_t dyn = (size_t)cfg.tbl_bytes[v] + (size_t)cpb * cb;
-        cudaFuncSetAttribute(cand_kernel_ptr(v, gl, cfg.tbl_smem[v]), cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(cand_kernel_ptr(v, gl, cfg.tbl_smem[v], (sh.mode & DFLOP_MODE_ORDER4) != 0),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dyn);
         const uint32_t want = (sh.n_cand + cpb - 1) / cpb;
         cfg.cpb[v] = cpb;
@@ -402,7 +405,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     uint8_t* slot_apos = reinterpret_cast<uint8_t*>(ws + cfg.o_slot_apos);
     uint16_t* slot_csr = reinterpret_cast<uint16_t*>(ws + cfg.o_slot_csr);
     const uint32_t n = a.sh.n;
-    const uint32_t allow_pack = a.sh.mode == DFLOP_MODE_EXHAUSTIVE ? 0u : 1u;
+    const uint32_t allow_pack = (a.sh.mode & DFLOP_MODE_EXHAUSTIVE) ? 0u : 1u;
 
     k_init<<<std::max(1u, std::min<uint32_t>((cfg.n_slots + 255) / 256, 148)), 256, 0, s>>>(hdr, slot_key,
                                                                                           cfg.n_slots);
@@ -445,11 +448,12 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     p.id_base = a.id_base;
     p.seed0 = a.seed0;
     p.seed1 = a.seed1;
-    p.exhaustive = a.sh.mode == DFLOP_MODE_EXHAUSTIVE;
+    p.exhaustive = (a.sh.mode & DFLOP_MODE_EXHAUSTIVE) ? 1u : 0u;
     p.wide = a.sh.m > 255;
     p.cap = cfg.cap;
     p.sigma = cfg.sigma;
     p.cnt_smem = cfg.cnt_smem ? 1u : 0u;
+    p.order4 = (a.sh.mode & DFLOP_MODE_ORDER4) ? 1u : 0u;
     p.csr_len = cfg.csr_len;
     p.apos_bytes = cfg.apos_bytes;
     p.phase = phase_counters();
@@ -469,7 +473,8 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
         L.grid = cfg.grid[v];
         L.cpb = cfg.cpb[v];
         L.dyn = (size_t)cfg.tbl_bytes[v] + (size_t)cfg.cpb[v] * cfg.cand_bytes[v];
-        cudaFuncSetAttribute(cand_kernel_ptr(v, cfg.gl, cfg.tbl_smem[v]), cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(cand_kernel_ptr(v, cfg.gl, cfg.tbl_smem[v], p.order4 != 0),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)L.dyn);
         cand_launch(L, q, s);
         prof_mark(mark, v + 1, s);

@@ -39,6 +39,7 @@ struct CandParams {
     uint32_t c_begin, c_end, id_base, seed0, seed1;
     uint32_t exhaustive, wide, cap, sigma, csr_len, apos_bytes, want_variant;
     uint32_t cnt_smem;           // refinement list counters in shared memory (else global)
+    uint32_t order4;             // DFLOP_MODE_ORDER4: best of four slot orders per replica
     uint32_t tbl_bytes, cand_bytes, off_fl, off_scr;
     unsigned long long* phase;   // diagnostic phase counters (timing builds), else null
 };
@@ -51,7 +52,7 @@ struct CandLaunch {
     size_t dyn;
 };
 
-const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem);
+const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem, bool o4);
 void cand_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 
 }  // namespace dflop

@@ -698,55 +698,104 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
 // the rest (LF, L-LF) (R7).  The host-built topological order is grouped in Kahn levels;
 // the GL lanes of the group run the ops of one level concurrently (distinct stages), rings
 // of depth D carry the end times between stages.
-template <typename A, bool PK, int GL>
-DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr,
-                         uint32_t gl) {
+template <typename A, bool PK, int GL, typename Map>
+DFLOP_DEV u64 score_replica(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr,
+                            uint32_t gl, uint32_t rho, Map&& slot_of) {
     const uint32_t S = p.S, D = p.D, Dm = p.D - 1;
     u64* last = scr;
     u64* FR = scr + S;
     u64* BR = FR + S * D;
+    for (uint32_t s = gl; s < S; s += GL) last[s] = 0;
+    __syncwarp(FULL);
+    uint32_t q0 = __ldg(p.levels);
+    for (uint32_t L = 0; L < p.n_levels; ++L) {
+        const uint32_t q1 = __ldg(p.levels + L + 1);
+        for (uint32_t q = q0 + gl; q < q1; q += GL) {
+            const uint32_t op = __ldg(p.ops + q);
+            const uint32_t kind = op_kind(op), s = op_stage(op), k = op_mb(op);
+            const uint32_t j = slot_of(k) * p.l_dp + rho;
+            const Pair2<A> el = EL[j], fl = FL[j];
+            const bool enc = s < p.e_pp;
+            u64 dur, dep = 0;
+            if (kind == 0) {
+                dur = enc ? (u64)fl.a : (u64)fl.b;
+                if (s > 0) dep = FR[(s - 1) * D + (k & Dm)];
+            } else {
+                dur = enc ? (u64)(unpack<A, PK>(el.a, sh) - fl.a) : (u64)(unpack<A, PK>(el.b, sh) - fl.b);
+                dep = (s + 1 < S) ? BR[(s + 1) * D + (k & Dm)] : FR[s * D + (k & Dm)];
+            }
+            const u64 l0 = last[s];
+            const u64 end = (l0 > dep ? l0 : dep) + dur;
+            last[s] = end;
+            if (kind == 0)
+                FR[s * D + (k & Dm)] = end;
+            else
+                BR[s * D + (k & Dm)] = end;
+        }
+        q0 = q1;
+        __syncwarp(FULL);
+    }
+    u64 t = 0;
+    for (uint32_t s = gl; s < S; s += GL) t = last[s] > t ? last[s] : t;
+    t = max_reduce<u64, GL>(t, FULL);
+    __syncwarp(FULL);
+    return t;
+}
+
+template <typename A, bool PK, int GL>
+DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr,
+                         uint32_t gl) {
     u64 T = 0;
     for (uint32_t rho = 0; rho < p.l_dp; ++rho) {
-        for (uint32_t s = gl; s < S; s += GL) last[s] = 0;
-        __syncwarp(FULL);
-        uint32_t q0 = __ldg(p.levels);
-        for (uint32_t L = 0; L < p.n_levels; ++L) {
-            const uint32_t q1 = __ldg(p.levels + L + 1);
-            for (uint32_t q = q0 + gl; q < q1; q += GL) {
-                const uint32_t op = __ldg(p.ops + q);
-                const uint32_t kind = op_kind(op), s = op_stage(op), k = op_mb(op);
-                const uint32_t j = k * p.l_dp + rho;
-                const Pair2<A> el = EL[j], fl = FL[j];
-                const bool enc = s < p.e_pp;
-                u64 dur, dep = 0;
-                if (kind == 0) {
-                    dur = enc ? (u64)fl.a : (u64)fl.b;
-                    if (s > 0) dep = FR[(s - 1) * D + (k & Dm)];
-                } else {
-                    dur = enc ? (u64)(unpack<A, PK>(el.a, sh) - fl.a) : (u64)(unpack<A, PK>(el.b, sh) - fl.b);
-                    dep = (s + 1 < S) ? BR[(s + 1) * D + (k & Dm)] : FR[s * D + (k & Dm)];
-                }
-                const u64 l0 = last[s];
-                const u64 end = (l0 > dep ? l0 : dep) + dur;
-                last[s] = end;
-                if (kind == 0)
-                    FR[s * D + (k & Dm)] = end;
-                else
-                    BR[s * D + (k & Dm)] = end;
+        const u64 t = score_replica<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [](uint32_t k) { return k; });
+        T = t > T ? t : T;
+    }
+    return T;
+}
+
+// N4(a) per candidate (DFLOP_MODE_ORDER4, R37): each replica under its best of the four start
+// orders of the order search (slot order, W = max(E, L) ascending, descending, valley); the
+// orders come from rank counts over the replica's slots (ties by slot, as the stable sorts
+// of orc_order_search).  Only in the O4 instantiations of the kernel.
+template <typename A, bool PK, int GL>
+DFLOP_DEV u64 score_order4(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL,
+                                        u64* scr, uint32_t gl) {
+    const uint32_t M = p.n_mb, half = (M + 1) / 2;
+    uint16_t* asc = reinterpret_cast<uint16_t*>(scr + (p.S + 2 * p.S * p.D));
+    uint16_t* desc = asc + M;
+    auto W = [&](uint32_t k, uint32_t rho) {
+        const Pair2<A> el = EL[k * p.l_dp + rho];
+        return unpack<A, PK>(maxa(el.a, el.b), sh);
+    };
+    u64 T = 0;
+    for (uint32_t rho = 0; rho < p.l_dp; ++rho) {
+        for (uint32_t k = gl; k < M; k += GL) {
+            const A wk = W(k, rho);
+            uint32_t ra = 0, rd = 0;
+            for (uint32_t k2 = 0; k2 < M; ++k2) {
+                const A w2 = W(k2, rho);
+                ra += (w2 < wk || (w2 == wk && k2 < k)) ? 1u : 0u;
+                rd += (w2 > wk || (w2 == wk && k2 < k)) ? 1u : 0u;
             }
-            q0 = q1;
-            __syncwarp(FULL);
+            asc[ra] = (uint16_t)k;
+            desc[rd] = (uint16_t)k;
         }
-        u64 t = 0;
-        for (uint32_t s = gl; s < S; s += GL) t = last[s] > t ? last[s] : t;
-        t = max_reduce<u64, GL>(t, FULL);
+        __syncwarp(FULL);
+        u64 t = score_replica<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [](uint32_t k) { return k; });
+        u64 t1 = score_replica<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [&](uint32_t k) { return (uint32_t)asc[k]; });
+        t = t1 < t ? t1 : t;
+        t1 = score_replica<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [&](uint32_t k) { return (uint32_t)desc[k]; });
+        t = t1 < t ? t1 : t;
+        t1 = score_replica<A, PK, GL>(p, sh, EL, FL, scr, gl, rho,
+                                      [&](uint32_t k) { return (uint32_t)asc[k < half ? 2 * k : 2 * (M - 1 - k) + 1]; });
+        t = t1 < t ? t1 : t;
         T = t > T ? t : T;
         __syncwarp(FULL);
     }
     return T;
 }
 
-template <typename A, bool PK, int GL, bool SM>
+template <typename A, bool PK, int GL, bool SM, bool O4>
 DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
                              Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, u64& Tc,
                              u64& cmax, PhaseTimer& ph) {
@@ -785,11 +834,14 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
     }
     cmax = (u64)max_reduce<A, GL>(cm, FULL);
     ph.mark(6);
-    Tc = score_1f1b<A, PK, GL>(p, sh, EL, FL, reinterpret_cast<u64*>(scr), gl);
+    if constexpr (O4)  // DFLOP_MODE_ORDER4: a separate kernel instantiation
+        Tc = score_order4<A, PK, GL>(p, sh, EL, FL, reinterpret_cast<u64*>(scr), gl);
+    else
+        Tc = score_1f1b<A, PK, GL>(p, sh, EL, FL, reinterpret_cast<u64*>(scr), gl);
     ph.mark(5);
 }
 
-template <typename A, bool PK, int GL, bool SM>
+template <typename A, bool PK, int GL, bool SM, bool O4>
 __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     if (p.hdr->variant != p.want_variant) return;  // another variant runs
     const uint32_t sh = PK ? p.hdr->shift : 0u;
@@ -835,7 +887,7 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         const uint32_t c = valid ? c0 + grp : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
         u64 Tc, cmax;
-        run_candidate<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, csr, gl, Tc, cmax, ph);
+        run_candidate<A, PK, GL, SM, O4>(p, T, c, sh, EL, FL, apos, scr, csr, gl, Tc, cmax, ph);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
         u64 key;
         if (Tc >= (1ull << 40)) {
@@ -868,36 +920,37 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     }
 }
 
-template <typename A, bool PK, bool SM>
+template <typename A, bool PK, bool SM, bool O4>
 static const void* ptr_gl(int gl) {
     switch (gl) {
-        case 1: return reinterpret_cast<const void*>(&k_candidates<A, PK, 1, SM>);
-        case 2: return reinterpret_cast<const void*>(&k_candidates<A, PK, 2, SM>);
-        case 4: return reinterpret_cast<const void*>(&k_candidates<A, PK, 4, SM>);
-        case 8: return reinterpret_cast<const void*>(&k_candidates<A, PK, 8, SM>);
-        case 16: return reinterpret_cast<const void*>(&k_candidates<A, PK, 16, SM>);
-        default: return reinterpret_cast<const void*>(&k_candidates<A, PK, 32, SM>);
+        case 1: return reinterpret_cast<const void*>(&k_candidates<A, PK, 1, SM, O4>);
+        case 2: return reinterpret_cast<const void*>(&k_candidates<A, PK, 2, SM, O4>);
+        case 4: return reinterpret_cast<const void*>(&k_candidates<A, PK, 4, SM, O4>);
+        case 8: return reinterpret_cast<const void*>(&k_candidates<A, PK, 8, SM, O4>);
+        case 16: return reinterpret_cast<const void*>(&k_candidates<A, PK, 16, SM, O4>);
+        default: return reinterpret_cast<const void*>(&k_candidates<A, PK, 32, SM, O4>);
     }
 }
 
-template <typename A, bool PK, bool SM>
+template <typename A, bool PK, bool SM, bool O4>
 static void launch_gl(const CandLaunch& L, const CandParams& p, cudaStream_t s) {
     const dim3 grid(L.grid), block(L.cpb * L.gl);
     switch (L.gl) {
-        case 1: k_candidates<A, PK, 1, SM><<<grid, block, L.dyn, s>>>(p); break;
-        case 2: k_candidates<A, PK, 2, SM><<<grid, block, L.dyn, s>>>(p); break;
-        case 4: k_candidates<A, PK, 4, SM><<<grid, block, L.dyn, s>>>(p); break;
-        case 8: k_candidates<A, PK, 8, SM><<<grid, block, L.dyn, s>>>(p); break;
-        case 16: k_candidates<A, PK, 16, SM><<<grid, block, L.dyn, s>>>(p); break;
-        default: k_candidates<A, PK, 32, SM><<<grid, block, L.dyn, s>>>(p); break;
+        case 1: k_candidates<A, PK, 1, SM, O4><<<grid, block, L.dyn, s>>>(p); break;
+        case 2: k_candidates<A, PK, 2, SM, O4><<<grid, block, L.dyn, s>>>(p); break;
+        case 4: k_candidates<A, PK, 4, SM, O4><<<grid, block, L.dyn, s>>>(p); break;
+        case 8: k_candidates<A, PK, 8, SM, O4><<<grid, block, L.dyn, s>>>(p); break;
+        case 16: k_candidates<A, PK, 16, SM, O4><<<grid, block, L.dyn, s>>>(p); break;
+        default: k_candidates<A, PK, 32, SM, O4><<<grid, block, L.dyn, s>>>(p); break;
     }
 }
 
-// one translation unit per (variant, table placement) so the 36 instantiations build in parallel
-#define DFLOP_CAND_UNIT(NAME, A, PK, SM)                                                         \
-    const void* cand_ptr_##NAME(int gl) { return ptr_gl<A, PK, SM>(gl); }                         \
+// one translation unit per (variant, table placement, ORDER4) so the 72 instantiations build
+// in parallel
+#define DFLOP_CAND_UNIT(NAME, A, PK, SM, O4)                                                     \
+    const void* cand_ptr_##NAME(int gl) { return ptr_gl<A, PK, SM, O4>(gl); }                     \
     void cand_launch_##NAME(const CandLaunch& L, const CandParams& p, cudaStream_t s) {           \
-        launch_gl<A, PK, SM>(L, p, s);                                                            \
+        launch_gl<A, PK, SM, O4>(L, p, s);                                                        \
     }
 
 }  // namespace dflop

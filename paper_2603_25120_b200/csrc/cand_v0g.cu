@@ -2,5 +2,5 @@
 #include "cand_impl.cuh"
 
 namespace dflop {
-DFLOP_CAND_UNIT(v0g, uint32_t, true, false)
+DFLOP_CAND_UNIT(v0g, uint32_t, true, false, false)
 }  // namespace dflop

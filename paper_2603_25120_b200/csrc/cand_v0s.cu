@@ -2,5 +2,5 @@
 #include "cand_impl.cuh"
 
 namespace dflop {
-DFLOP_CAND_UNIT(v0s, uint32_t, true, true)
+DFLOP_CAND_UNIT(v0s, uint32_t, true, true, false)
 }  // namespace dflop

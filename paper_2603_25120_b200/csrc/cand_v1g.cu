@@ -2,5 +2,5 @@
 #include "cand_impl.cuh"
 
 namespace dflop {
-DFLOP_CAND_UNIT(v1g, uint32_t, false, false)
+DFLOP_CAND_UNIT(v1g, uint32_t, false, false, false)
 }  // namespace dflop

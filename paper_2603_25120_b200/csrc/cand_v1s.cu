@@ -2,5 +2,5 @@
 #include "cand_impl.cuh"
 
 namespace dflop {
-DFLOP_CAND_UNIT(v1s, uint32_t, false, true)
+DFLOP_CAND_UNIT(v1s, uint32_t, false, true, false)
 }  // namespace dflop

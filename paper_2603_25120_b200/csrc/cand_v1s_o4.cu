@@ -1,0 +1,6 @@
+// cand_v1s_o4.cu -- instantiation unit of the candidate kernel (see cand_impl.cuh)
+#include "cand_impl.cuh"
+
+namespace dflop {
+DFLOP_CAND_UNIT(v1s_o4, uint32_t, false, true, true)
+}  // namespace dflop

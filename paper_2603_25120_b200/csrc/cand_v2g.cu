@@ -2,5 +2,5 @@
 #include "cand_impl.cuh"
 
 namespace dflop {
-DFLOP_CAND_UNIT(v2g, u64, false, false)
+DFLOP_CAND_UNIT(v2g, u64, false, false, false)
 }  // namespace dflop

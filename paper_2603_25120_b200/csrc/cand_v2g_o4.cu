@@ -1,0 +1,6 @@
+// cand_v2g_o4.cu -- instantiation unit of the candidate kernel (see cand_impl.cuh)
+#include "cand_impl.cuh"
+
+namespace dflop {
+DFLOP_CAND_UNIT(v2g_o4, u64, false, false, true)
+}  // namespace dflop

@@ -2,5 +2,5 @@
 #include "cand_impl.cuh"
 
 namespace dflop {
-DFLOP_CAND_UNIT(v2s, u64, false, true)
+DFLOP_CAND_UNIT(v2s, u64, false, true, false)
 }  // namespace dflop

@@ -5,18 +5,35 @@ namespace dflop {
 
 const void* cand_ptr_v0s(int gl);
 void cand_launch_v0s(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+const void* cand_ptr_v0s_o4(int gl);
+void cand_launch_v0s_o4(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 const void* cand_ptr_v0g(int gl);
 void cand_launch_v0g(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+const void* cand_ptr_v0g_o4(int gl);
+void cand_launch_v0g_o4(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 const void* cand_ptr_v1s(int gl);
 void cand_launch_v1s(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+const void* cand_ptr_v1s_o4(int gl);
+void cand_launch_v1s_o4(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 const void* cand_ptr_v1g(int gl);
 void cand_launch_v1g(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+const void* cand_ptr_v1g_o4(int gl);
+void cand_launch_v1g_o4(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 const void* cand_ptr_v2s(int gl);
 void cand_launch_v2s(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+const void* cand_ptr_v2s_o4(int gl);
+void cand_launch_v2s_o4(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 const void* cand_ptr_v2g(int gl);
 void cand_launch_v2g(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+const void* cand_ptr_v2g_o4(int gl);
+void cand_launch_v2g_o4(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 
-const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem) {
+const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem, bool o4) {
+    if (o4) switch (variant) {
+            case 0: return tbl_smem ? cand_ptr_v0s_o4(gl) : cand_ptr_v0g_o4(gl);
+            case 1: return tbl_smem ? cand_ptr_v1s_o4(gl) : cand_ptr_v1g_o4(gl);
+            default: return tbl_smem ? cand_ptr_v2s_o4(gl) : cand_ptr_v2g_o4(gl);
+        }
     switch (variant) {
         case 0: return tbl_smem ? cand_ptr_v0s(gl) : cand_ptr_v0g(gl);
         case 1: return tbl_smem ? cand_ptr_v1s(gl) : cand_ptr_v1g(gl);
@@ -25,6 +42,14 @@ const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem) {
 }
 
 void cand_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s) {
+    if (p.order4) {
+        switch (L.variant) {
+            case 0: L.tbl_smem ? cand_launch_v0s_o4(L, p, s) : cand_launch_v0g_o4(L, p, s); break;
+            case 1: L.tbl_smem ? cand_launch_v1s_o4(L, p, s) : cand_launch_v1g_o4(L, p, s); break;
+            default: L.tbl_smem ? cand_launch_v2s_o4(L, p, s) : cand_launch_v2g_o4(L, p, s); break;
+        }
+        return;
+    }
     switch (L.variant) {
         case 0: L.tbl_smem ? cand_launch_v0s(L, p, s) : cand_launch_v0g(L, p, s); break;
         case 1: L.tbl_smem ? cand_launch_v1s(L, p, s) : cand_launch_v1g(L, p, s); break;

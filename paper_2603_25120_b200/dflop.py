@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DFLOP_LIB") or os.path.join(HERE, "libdflop.so")
 
 MAX_X, MAX_TP = 32, 4
-MODE_HEURISTIC, MODE_EXHAUSTIVE = 0, 1
+MODE_HEURISTIC, MODE_EXHAUSTIVE, MODE_ORDER4 = 0, 1, 16
 SEARCH_FIXED, SEARCH_ALG1 = 0, 1
 DEV_COST_OVERFLOW, DEV_MAKESPAN_OVERFLOW = 1, 2
 STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE", 3: "OVERFLOW", 4: "INFEASIBLE", 5: "CUDA", 6: "NCCL",
@@ -351,14 +351,14 @@ def index_groups(assign, m: int, stream=None):
 def search_plans(model: Dict, tiles, frames, text, K: int, R: int, G: int, seed: Sequence[int],
                  plan: Optional[Dict] = None, cluster: Optional[Dict] = None, mem: Optional[Dict] = None,
                  gbs: int = 0, top_p: int = 1, comm=None, want_assign: bool = True, stage_a_out=None,
-                 ws: Optional[Workspace] = None, stream=None) -> Dict:
+                 ws: Optional[Workspace] = None, stream=None, order4: bool = False) -> Dict:
     """a1-a6 for one global batch (synchronous).  ``plan`` given -> FIXED mode; else Algorithm 1."""
     import torch
     n = tiles.numel()
     dev = tiles.device
     sp = SearchParams()
     sp.struct_size = C.sizeof(SearchParams)
-    sp.mode = SEARCH_FIXED if plan is not None else SEARCH_ALG1
+    sp.mode = (SEARCH_FIXED if plan is not None else SEARCH_ALG1) | (MODE_ORDER4 if order4 else 0)
     if plan is not None:
         sp.fixed_plan = plan_struct(plan)
     sp.gbs, sp.top_p, sp.K, sp.R, sp.G = gbs, top_p, K, R, G
@@ -465,7 +465,8 @@ def route_plan(cost_ticks, plan: Dict, assign, ws: Optional[Workspace] = None, s
 def search_plans_batches(model: Dict, tiles, frames, text, batch_offsets: Sequence[int], K: int, R: int, G: int,
                          seed: Sequence[int], plan: Optional[Dict] = None, cluster: Optional[Dict] = None,
                          mem: Optional[Dict] = None, gbs: int = 0, top_p: int = 1, comm=None,
-                         want_assign: bool = True, ws: Optional[Workspace] = None, stream=None) -> Dict:
+                         want_assign: bool = True, ws: Optional[Workspace] = None, stream=None,
+                         order4: bool = False) -> Dict:
     """N2, Eq. (1) over a sample of D batches (synchronous): batch b = samples
     [batch_offsets[b], batch_offsets[b+1]) of the concatenated features; its family uses
     Philox key (seed[0], seed[1] + b).  Returns the dflop_plan_result fields (makespan =
@@ -477,7 +478,7 @@ def search_plans_batches(model: Dict, tiles, frames, text, batch_offsets: Sequen
     dev = tiles.device
     sp = SearchParams()
     sp.struct_size = C.sizeof(SearchParams)
-    sp.mode = SEARCH_FIXED if plan is not None else SEARCH_ALG1
+    sp.mode = (SEARCH_FIXED if plan is not None else SEARCH_ALG1) | (MODE_ORDER4 if order4 else 0)
     if plan is not None:
         sp.fixed_plan = plan_struct(plan)
     sp.gbs, sp.top_p, sp.K, sp.R, sp.G = gbs, top_p, K, R, G

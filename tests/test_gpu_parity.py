@@ -373,3 +373,30 @@ def test_global_item_table_path(D, O, presets):
     _, q, st, _ = O.predict(p.model, p.plan, t, f, x)
     assert st == 0
     check_balance(D, O, q, p.plan, 4096, 4, p.G, p.seed(4), 100, 148)
+
+
+@pytest.mark.parametrize("k, over, c0, c1", [(2, None, 0, 512), (3, None, 0, 128), (5, None, 0, 16),
+                                            (2, dict(l_dp=2, n_mb=8), 0, 256)])
+def test_order4_mode_parity(D, O, presets, k, over, c0, c1):
+    """DFLOP_MODE_ORDER4 (N4(a) per candidate, R37): per-candidate T bit-exact against the
+    oracle's ORDER4 mode, never above the slot-order T."""
+    p = presets[k]
+    pl = dict(p.plan, **over) if over else p.plan
+    (t, f, x), (dt, df, dx) = feats(p)
+    _, ticks = D.predict_costs(p.model, pl, dt, df, dx, want_f32=False)
+    q = host_u32(ticks)
+    g, o = check_balance(D, O, q, pl, p.K, p.R, p.G, p.seed(0), c0, c1, mode=16)
+    g0 = gpu_balance(D, dev_u32(q), pl, p.K, p.R, p.G, p.seed(0), c0, c1)
+    assert (g["cT"] <= g0["cT"]).all() and (g["cC"] == g0["cC"]).all()
+
+
+def test_order4_search_and_winner_order(D, O, presets):
+    p = presets[3]
+    (t, f, x), (dt, df, dx) = feats(p)
+    res = D.search_plans(p.model, dt, df, dx, K=1024, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan, order4=True)
+    _, ticks = D.predict_costs(p.model, p.plan, dt, df, dx, want_f32=False)
+    o = O.balance_threaded(host_u32(ticks), p.plan, 1024, p.R, p.G, p.seed(0), mode=16, per_candidate=False)
+    assert res["makespan"] == o["T"] and res["cand"] == o["c"]
+    # the winner's slot orders: the rounds = 0 order search of its assignment
+    g = D.order_search(ticks, p.plan, res["assign"], rounds=0)
+    assert g["makespan"] == res["makespan"]

@@ -20,6 +20,7 @@ ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--K", type=int, default=8192)
 ap.add_argument("--R", type=int, default=-1)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--mode", type=int, default=0, help="16 = DFLOP_MODE_ORDER4")
 a = ap.parse_args()
 p = synth.presets()[a.config]
 R = p.R if a.R < 0 else a.R
@@ -29,7 +30,7 @@ for rep in range(a.reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    r = D.balance_microbatches(ticks, p.plan, a.K, R, p.G, p.seed(0))
+    r = D.balance_microbatches(ticks, p.plan, a.K, R, p.G, p.seed(0), mode=a.mode)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
