@@ -335,27 +335,39 @@ DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t es, 
 }
 
 // Two consecutive samples A, B of the (perturbed) order in one step of the packed variant
-// with 8 buckets per lane -- exactly the sequential decisions: B's argmin is computed on the
+// -- exactly the sequential decisions: B's argmin is computed on the
 // loads before A's update together with its runner-up; A's update only raises bucket a*, so
 // if B's best b1 is not a* it stays B's argmin (ties: the packed keys carry the index), and
 // if b1 = a*, B's argmin is the smaller of the runner-up and a*'s key after A's update
 // (computed by a*'s owner lane and broadcast).  Halves the dependent reduction chains.
-template <int GL>
+// FIX8: m == 8 * GL and a one-byte assignment (every preset); else any m (loop, bounds).
+template <int GL, bool FIX8>
 DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* apos, uint32_t pa, uint32_t pb,
                              const ItemRec<uint32_t>& ia, const ItemRec<uint32_t>& ib, uint32_t use, uint32_t jmask,
-                             uint32_t gl, uint32_t lane) {
+                             uint32_t gl, uint32_t lane, uint32_t m, bool wide) {
     const uint32_t esa = ia.e & use, lsa = ia.l & use, esb = ib.e & use, lsb = ib.l & use;
     uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+    if constexpr (FIX8) {
 #pragma unroll
-    for (uint32_t k = 0; k < 8; k += 2) {
-        const Pair2<uint32_t> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
-        a0 = min(a0, max(x.a + esa, x.b + lsa));
-        a1 = min(a1, max(y.a + esa, y.b + lsa));
-        const uint32_t vx = max(x.a + esb, x.b + lsb), vy = max(y.a + esb, y.b + lsb);
-        m2 = min(m2, max(m1, vx));
-        m1 = min(m1, vx);
-        m2 = min(m2, max(m1, vy));
-        m1 = min(m1, vy);
+        for (uint32_t k = 0; k < 8; k += 2) {
+            const Pair2<uint32_t> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
+            a0 = min(a0, max(x.a + esa, x.b + lsa));
+            a1 = min(a1, max(y.a + esa, y.b + lsa));
+            const uint32_t vx = max(x.a + esb, x.b + lsb), vy = max(y.a + esb, y.b + lsb);
+            m2 = min(m2, max(m1, vx));
+            m1 = min(m1, vx);
+            m2 = min(m2, max(m1, vy));
+            m1 = min(m1, vy);
+        }
+    } else {
+#pragma unroll 2
+        for (uint32_t j = gl; j < m; j += GL) {
+            const Pair2<uint32_t> x = EL[j];
+            a0 = min(a0, max(x.a + esa, x.b + lsa));
+            const uint32_t vx = max(x.a + esb, x.b + lsb);
+            m2 = min(m2, max(m1, vx));
+            m1 = min(m1, vx);
+        }
     }
     uint32_t ba = min(a0, a1);
 #pragma unroll
@@ -379,13 +391,19 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
         EL[ja] = Pair2<uint32_t>{ela.a + ia.e, ela.b + ia.l};
         Pair2<uint32_t> fl = FL[ja];
         FL[ja] = Pair2<uint32_t>{fl.a + ia.ef, fl.b + ia.lf};
-        apos[pa] = (uint8_t)ja;
+        if constexpr (FIX8)
+            apos[pa] = (uint8_t)ja;
+        else
+            set_apos(apos, pa, ja, wide);
     }
     if ((jb & (GL - 1)) == gl) {  // after A's update in program order when jb = ja (same lane)
         const Pair2<uint32_t> el = EL[jb], fl = FL[jb];
         EL[jb] = Pair2<uint32_t>{el.a + ib.e, el.b + ib.l};
         FL[jb] = Pair2<uint32_t>{fl.a + ib.ef, fl.b + ib.lf};
-        apos[pb] = (uint8_t)jb;
+        if constexpr (FIX8)
+            apos[pb] = (uint8_t)jb;
+        else
+            set_apos(apos, pb, jb, wide);
     }
 }
 
@@ -412,12 +430,22 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
         uint32_t t = 0;
 #ifndef DFLOP_NO_LPT_PAIRS
         if constexpr (PK) {
-            if (m == 8 * GL && !wide) {  // two samples per step (see lpt_pair_step; u8 assignment)
+            // two samples per step (see lpt_pair_step)
+            if (m == 8 * GL && !wide) {
                 for (; t + 1 < ng; t += 2) {
                     const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
-                    lpt_pair_step<GL>(reinterpret_cast<Pair2<uint32_t>*>(EL), reinterpret_cast<Pair2<uint32_t>*>(FL),
-                                      apos, pa, pb, T.item(pa), T.item(pb), (uint32_t)use, jmask, gl, lane);
+                    lpt_pair_step<GL, true>(reinterpret_cast<Pair2<uint32_t>*>(EL),
+                                            reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.item(pa),
+                                            T.item(pb), (uint32_t)use, jmask, gl, lane, m, false);
+                }
+            } else {
+                for (; t + 1 < ng; t += 2) {
+                    const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
+                    const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
+                    lpt_pair_step<GL, false>(reinterpret_cast<Pair2<uint32_t>*>(EL),
+                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.item(pa),
+                                             T.item(pb), (uint32_t)use, jmask, gl, lane, m, wide);
                 }
             }
         }
