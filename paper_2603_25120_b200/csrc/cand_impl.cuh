@@ -590,7 +590,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         ph.mark(2);
         A bsc = amax<A>();
         uint32_t bi = 0xFFFFFFFFu, brk = 0xFFFFFFFFu;
-        u64 bkey = ~0ull;  // 32-bit scores: (score << 32 | item << 16 | rank), branch-free minima
+        u64 bkey = ~0ull;  // 32-bit scores: (row minimum << 32 | item), branch-free minima
         const uint32_t nBs = min(nB, cap);
         // all (i, i') with i in j*, i' in {NONE} u j'; lexicographic min of (score, i, rank(i'))
         // two j* members per lane and step: every j' member loaded once serves two pairs
@@ -617,22 +617,22 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 pl1 = pl0;
             }
             const A n0 = maxa(maxa(se0, sl0), maxa(pe0, pl0)), n1 = maxa(maxa(se1, sl1), maxa(pe1, pl1));
-            // 32-bit scores: per row the minimum of (score << 32 | rank) (rank 0 = NONE), the
-            // item index is or-ed in once per row below
-            u64 r0 = (u64)n0 << 32, r1 = (u64)n1 << 32;
+            // 32-bit scores, phase 1: per row only the minimum score (the NONE pair included);
+            // the rank of the winning partner is found afterwards for the one winning row
+            uint32_t r0 = (uint32_t)n0, r1 = (uint32_t)n1;
             if (sizeof(A) != 4) {
                 lex_update(bsc, bi, brk, n0, i0, 0u);
                 lex_update(bsc, bi, brk, n1, i1, 0u);
             }
             auto pair = [&](uint32_t pj) {
                 const Pair2<A> b = T.el(pj);
-                const uint32_t rk = T.idx(pj) + 1u;
                 const A s0 = maxa(maxa<A>(se0 + b.a, sl0 + b.b), maxa<A>(pe0 - b.a, pl0 - b.b));
                 const A s1 = maxa(maxa<A>(se1 + b.a, sl1 + b.b), maxa<A>(pe1 - b.a, pl1 - b.b));
                 if (sizeof(A) == 4) {
-                    r0 = min(r0, pack64((uint32_t)s0, rk));
-                    r1 = min(r1, pack64((uint32_t)s1, rk));
+                    r0 = min(r0, (uint32_t)s0);
+                    r1 = min(r1, (uint32_t)s1);
                 } else {
+                    const uint32_t rk = T.idx(pj) + 1u;
                     lex_update(bsc, bi, brk, s0, i0, rk);
                     lex_update(bsc, bi, brk, s1, i1, rk);
                 }
@@ -655,17 +655,38 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 pair(q3);
             }
             for (v = max(v, cap); v < nB; ++v) pair(__ldcg(gsp + v));
-            if (sizeof(A) == 4)  // (score, item, rank): the rank field is 16 bits (n <= 65535)
-                bkey = min(bkey, min(r0 | ((u64)i0 << 16), r1 | ((u64)i1 << 16)));
+            if (sizeof(A) == 4)  // (row minimum, item): lexicographic over the lane's rows
+                bkey = min(bkey, min(pack64(r0, i0), pack64(r1, i1)));
         }
         ph.mark(3);
         if (sizeof(A) == 4) {
 #pragma unroll
             for (int off = GL / 2; off > 0; off >>= 1) bkey = min(bkey, __shfl_xor_sync(FULL, bkey, off));
-            if (bkey != ~0ull) {
-                bsc = (A)(bkey >> 32);
-                bi = (uint32_t)(bkey >> 16) & 0xFFFFu;
-                brk = (uint32_t)bkey & 0xFFFFu;
+            // phase 2 (only when the move would be applied): the least rank among the partners
+            // of the winning row that reach the minimum -- the same lexicographic minimum
+            // (score, i, rank) as one pass over 64-bit keys
+            const bool need = apply && bkey != ~0ull && (A)(bkey >> 32) < Ws;
+            if (__any_sync(FULL, need)) {  // warp-uniform (the reduction below shuffles)
+                const uint32_t S = (uint32_t)(bkey >> 32), istar = (uint32_t)bkey;
+                uint32_t rb = 0xFFFFFFFFu;
+                if (need) {
+                    const Pair2<A> a = T.el(__ldg(p.item_pos + istar));
+                    const A se = Bs.a - a.a, sl = Bs.b - a.b, pe = Bp.a + a.a, pl = Bp.b + a.b;
+                    if (gl == 0 && (uint32_t)maxa(maxa(se, sl), maxa(pe, pl)) == S) rb = 0;
+                    for (uint32_t v = gl; v < nB; v += GL) {
+                        const uint32_t pj = v < cap ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v);
+                        const Pair2<A> b = T.el(pj);
+                        const A sc = maxa(maxa<A>(se + b.a, sl + b.b), maxa<A>(pe - b.a, pl - b.b));
+                        if ((uint32_t)sc == S) rb = min(rb, T.idx(pj) + 1u);
+                    }
+                }
+#pragma unroll
+                for (int off = GL / 2; off > 0; off >>= 1) rb = min(rb, __shfl_xor_sync(FULL, rb, off));
+                if (need) {
+                    bsc = (A)S;
+                    bi = istar;
+                    brk = rb;
+                }
             }
         } else {
             lexmin_reduce<A, GL>(bsc, bi, brk, FULL);
