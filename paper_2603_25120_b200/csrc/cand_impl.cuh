@@ -348,17 +348,22 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
     const uint32_t esa = ia.e & use, lsa = ia.l & use, esb = ib.e & use, lsb = ib.l & use;
     uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
     if constexpr (FIX8) {
+        // B's two smallest of 8 keys by a merge tree: sorted pairs, then (lo, hi) merges
+        // m1 = min(lo, lo'), m2 = min(max(lo, lo'), hi, hi') -- 17 min/max instead of 24
+        uint32_t lo[4], hi[4];
 #pragma unroll
         for (uint32_t k = 0; k < 8; k += 2) {
             const Pair2<uint32_t> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
             a0 = min(a0, max(x.a + esa, x.b + lsa));
             a1 = min(a1, max(y.a + esa, y.b + lsa));
             const uint32_t vx = max(x.a + esb, x.b + lsb), vy = max(y.a + esb, y.b + lsb);
-            m2 = min(m2, max(m1, vx));
-            m1 = min(m1, vx);
-            m2 = min(m2, max(m1, vy));
-            m1 = min(m1, vy);
+            lo[k / 2] = min(vx, vy);
+            hi[k / 2] = max(vx, vy);
         }
+        const uint32_t l01 = min(lo[0], lo[1]), h01 = min(max(lo[0], lo[1]), min(hi[0], hi[1]));
+        const uint32_t l23 = min(lo[2], lo[3]), h23 = min(max(lo[2], lo[3]), min(hi[2], hi[3]));
+        m1 = min(l01, l23);
+        m2 = min(max(l01, l23), min(h01, h23));
     } else {
 #pragma unroll 2
         for (uint32_t j = gl; j < m; j += GL) {
