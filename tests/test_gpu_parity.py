@@ -400,3 +400,37 @@ def test_order4_search_and_winner_order(D, O, presets):
     # the winner's slot orders: the rounds = 0 order search of its assignment
     g = D.order_search(ticks, p.plan, res["assign"], rounds=0)
     assert g["makespan"] == res["makespan"]
+
+
+def test_fuzz_random_shapes(D, O):
+    """Random shapes through every balance code path (packed / plain / 64-bit variants, narrow
+    and wide assignments, one- and two-sample LPT steps, CSR overflow and rebuilds, ORDER4)
+    against the oracle, per candidate."""
+    rng = np.random.default_rng(2026)
+    for trial in range(80):
+        n_mb = int(rng.choice([1, 2, 3, 5, 8, 16, 33, 64, 150]))
+        l_dp = int(rng.choice([1, 1, 2, 3]))
+        e_pp, l_pp = int(rng.integers(1, 4)), int(rng.integers(1, 6))
+        pl = dict(e_tp=1, e_pp=e_pp, e_dp=1, l_tp=1, l_pp=l_pp, l_dp=l_dp, n_mb=n_mb)
+        m = n_mb * l_dp
+        n = int(rng.integers(0, 900))
+        hi = int(rng.choice([50, 5000, 2 ** 20, 2 ** 27]))   # 2^27: 64-bit sums, makespans < 2^40
+        q = rng.integers(0, hi, (4, n), dtype=np.uint64).astype(np.uint32)
+        if rng.random() < 0.3 and n:                          # heavy tail
+            q[:, rng.integers(0, n)] = np.uint32(min(hi * 40, 2 ** 31))
+        G = int(rng.choice([1, 4, 8, 16]))
+        R = int(rng.choice([0, 1, 6, 16]))
+        mode = int(rng.choice([0, 0, 16]))
+        K = 96
+        c0 = int(rng.integers(0, K - 24))
+        check_balance(D, O, q, pl, K, R, G, (trial, 7), c0, c0 + 24, mode=mode)
+
+
+def test_makespan_overflow_flag(D):
+    """Makespans >= 2^40 ticks do not fit the packed argmin key: the device status carries
+    DFLOP_DEV_MAKESPAN_OVERFLOW (include/dflop.h) and the search reports OVERFLOW."""
+    rng = np.random.default_rng(1)
+    pl = dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=2, l_dp=1, n_mb=4)
+    q = rng.integers(2 ** 30, 2 ** 31, (4, 2000), dtype=np.uint64).astype(np.uint32)
+    r = D.balance_microbatches(dev_u32(q), pl, 64, 2, 8, (1, 1))
+    assert D.cand_result(r["best"])["status"] & D.DEV_MAKESPAN_OVERFLOW
