@@ -50,9 +50,9 @@ def dist_env():
 def workload(args, world):
     from paper_2603_25120_b200 import synth
     p = synth.presets()[args.config]
-    if p.plan is None:
-        raise SystemExit("config 4 (Algorithm-1 search) is benchmarked with --config 4 via tests; use 1,2,3,5")
     K = args.K or p.K
+    if p.plan is None:  # config 4: the Algorithm-1 search (Stage A + P plans x K candidates)
+        return p, K, "strong", None, None
     scaling = "strong"
     if p.K_scaling == "weak":
         K = K * world
@@ -139,18 +139,28 @@ def oracle_rate(p, K_family, budget_s, threads=None):
     threads = threads or os.cpu_count() or 1
     t, f, x = p.features(0)
     t0 = time.perf_counter()
-    _, q, st, _ = O.predict(p.model, p.plan, t, f, x)
+    plan, what = p.plan, ""
+    if plan is None:  # Algorithm 1: the oracle's own Stage A, then the leader plan's family
+        mb, msq = O.batch_means(p.model, t, f, x)
+        T_A, cfgs = O.stage_a_all(p.model, p.mem(), p.cluster["n_gpus"], p.cluster["gpus_per_node"], p.gbs, mb, msq)
+        e, i = O.pair_to_config(cfgs, p.gbs, O.stage_a_top(T_A, 1)[0])
+        c = cfgs[e]
+        plan = dict(e_tp=int(c[0]), e_pp=int(c[1]), e_dp=int(c[2]), l_tp=int(c[3]), l_pp=int(c[4]), l_dp=int(c[5]),
+                    n_mb=i)
+        what = " (Stage A over all pairs, then the Stage-A leader plan's family)"
+    _, q, st, _ = O.predict(p.model, plan, t, f, x)
     done = 0
     chunk = threads * 8
     while True:
         c1 = min(K_family, done + chunk)
-        O.balance_threaded(q, p.plan, K_family, p.R, p.G, p.seed(0), done, c1, threads=threads, per_candidate=False)
+        O.balance_threaded(q, plan, K_family, p.R, p.G, p.seed(0), done, c1, threads=threads, per_candidate=False)
         done = c1
         dt = time.perf_counter() - t0
         if dt >= budget_s or done >= K_family:
             break
         chunk = min(max(chunk, int(done / dt * 2.0)), threads * 4096)
-    return done / dt, f"candidates [0, {done}) of batch 0 (+ predict of all {p.n} samples), {dt:.1f} s", threads
+    return (done / dt, f"candidates [0, {done}) of batch 0 (+ predict of all {p.n} samples){what}, {dt:.1f} s",
+            threads)
 
 
 def run_reference(args):
@@ -210,10 +220,20 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    alg1 = p.plan is None
+    P = p.top_p if alg1 else 1
+
+    def search(t, f, x, b):
+        if alg1:  # Algorithm 1: Stage A on the batch, Stage B over the top-P plans
+            return D.search_plans_batches(p.model, t, f, x, [0, p.n], K=K, R=p.R, G=p.G, seed=p.seed(b), comm=comm,
+                                          cluster=p.cluster, mem=p.mem(), gbs=p.gbs, top_p=P, ws=ws,
+                                          order4=args.order4)
+        return D.search_plans(p.model, t, f, x, K=K, R=p.R, G=p.G, seed=p.seed(b), plan=p.plan,
+                              comm=comm, want_assign=True, ws=ws, order4=args.order4)
+
     def step(b):
         t, f, x = dfeat[b % n_batches]
-        return D.search_plans(p.model, t, f, x, K=K, R=p.R, G=p.G, seed=p.seed(b % n_batches), plan=p.plan,
-                              comm=comm, want_assign=True, ws=ws, order4=args.order4)
+        return search(t, f, x, b % n_batches)
 
     for i in range(max(3, args.warmup)):
         step(i)
@@ -247,7 +267,7 @@ def main():
         lat = torch.tensor(times, dtype=torch.float64, device=dev)
         dist.all_reduce(lat, op=dist.ReduceOp.MAX)
         times = lat.tolist()
-    value = K * args.steps / (total_ms / 1e3)          # whole-job candidates per second
+    value = P * K * args.steps / (total_ms / 1e3)      # whole-job candidates per second
     ms_per_step = total_ms / args.steps
     p50 = statistics.median(times)
     p99 = float(np.percentile(np.array(times), 99))
@@ -265,8 +285,7 @@ def main():
             e0.record(stream)
             for d_, h_ in zip(dbuf, pinned[i % n_batches]):
                 d_.copy_(h_, non_blocking=True)
-            r = D.search_plans(p.model, *dbuf, K=K, R=p.R, G=p.G, seed=p.seed(i % n_batches), plan=p.plan,
-                               comm=comm, want_assign=True, ws=ws, order4=args.order4)
+            r = search(*dbuf, i % n_batches)
             out_host.copy_(r["assign"], non_blocking=True)
             e1.record(stream)
             e1.synchronize()
@@ -277,13 +296,23 @@ def main():
             tt = torch.tensor([e_total], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_total = float(tt.item())
-        e2e = {"value": K * len(e_times) / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": 3 * 4 * p.n,
+        e2e = {"value": P * K * len(e_times) / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": 3 * 4 * p.n,
                "d2h_bytes_per_step": 4 * p.n + 32 + 8, "p50_ms": statistics.median(e_times)}
 
     # ---- roofline of the dominant kernel (candidates: integer-issue bound)
     b, e = (K * rank) // world, (K * (rank + 1)) // world
-    ops_launch = algorithmic_ops_per_candidate(p.n, m, S, p.R, p.G) * (e - b)
-    cand_ms = prof["cand_ms"] / max(1, prof["cand_launches"])
+    if alg1:
+        # P plans of different shapes overlap on the Stage-B streams: their summed algorithmic
+        # work over the step's device time (a lower bound of the kernels' own rate)
+        plans = res["plans"]
+        ops_step = sum(algorithmic_ops_per_candidate(p.n, q["n_mb"] * q["l_dp"], q["e_pp"] + q["l_pp"], p.R, p.G)
+                       for q in plans) * (e - b)
+        m = sum(q["n_mb"] * q["l_dp"] for q in plans) / max(1, len(plans))
+        S = None
+        ops_launch, cand_ms = ops_step, ms_per_step
+    else:
+        ops_launch = algorithmic_ops_per_candidate(p.n, m, S, p.R, p.G) * (e - b)
+        cand_ms = prof["cand_ms"] / max(1, prof["cand_launches"])
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
@@ -294,7 +323,10 @@ def main():
                 "unit": "Tops/s", "frac": achieved / peak_tops, "traffic": None,
                 "kernel_ms": cand_ms, "kernel_share_of_step": cand_ms / ms_per_step,
                 "peak_note": f"{n_sm} SM x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
-                "ops_per_candidate": algorithmic_ops_per_candidate(p.n, m, S, p.R, p.G)}
+                "ops_per_candidate": ops_launch / max(1, (e - b) * P)}
+    if alg1:
+        roofline["kernel"] = "k_candidates<u32> x P plans (Stage B, 4 streams)"
+        roofline["duration_note"] = "device step time (Stage A + Stage B)"
     # traffic: dram__bytes_read.sum + dram__bytes_write.sum of the candidate kernel from the
     # committed ncu --set full capture (profiles/traffic.json), per candidate x this launch's K
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
@@ -314,8 +346,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "K_per_gpu": K // world, "order4": bool(args.order4), "R": p.R,
-                   "G": p.G, "plan": p.plan, "tick_ns": p.model["tick_ns"],
+        "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "K_per_gpu": K // world,
+                   "plans": P, "order4": bool(args.order4), "R": p.R,
+                   "G": p.G, "plan": p.plan if not alg1 else res["plan"], "tick_ns": p.model["tick_ns"],
                    "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"candidate-shard x{world}"},
         "p50_plan_latency_ms": p50, "p99_plan_latency_ms": p99,
         "candidate_microbatches_per_s": value * m,

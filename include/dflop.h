@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DFLOP_ABI_VERSION 2u
+#define DFLOP_ABI_VERSION 3u
 
 typedef int32_t dflop_status;
 #define DFLOP_OK 0
@@ -415,6 +415,8 @@ dflop_status dflop_route_plan(const uint32_t* cost_ticks, uint32_t n, const dflo
  *   batch_results  host dflop_cand_result[D] or NULL: theta*'s winner per batch.
  *   plan_objective host u64[top_p] or NULL: sum_b T_B(b) per Stage-B plan (Stage-A rank
  *                  order; UINT64_MAX when a plan had no candidate).
+ *   plans_out      host dflop_plan[top_p] or NULL: the Stage-B plans in Stage-A rank order
+ *                  (FIXED mode: the one fixed plan).
  *   assign         device u32 [total] or NULL: every batch's winning assignment.
  * Multi-GPU: candidates sharded as in dflop_search_plans; one NCCL min all-reduce of the
  * [P x D] key array, then one broadcast per batch from its winner's owner.  Errors as
@@ -424,7 +426,8 @@ dflop_status dflop_search_plans_batches(const dflop_cluster* cl, const dflop_cos
                                         const uint32_t* text, const uint32_t* batch_offsets, uint32_t n_batches,
                                         const dflop_search_params* sp, dflop_comm* comm, void* ws, size_t* ws_bytes,
                                         dflop_plan_result* out, dflop_cand_result* batch_results,
-                                        uint64_t* plan_objective, uint32_t* assign, dflop_stream_t stream);
+                                        uint64_t* plan_objective, dflop_plan* plans_out, uint32_t* assign,
+                                        dflop_stream_t stream);
 
 /* ---------------------------------------------------------------- NCCL
  * Bootstrap: rank 0 calls dflop_get_unique_id, the caller broadcasts the 128 bytes

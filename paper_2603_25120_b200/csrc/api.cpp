@@ -542,7 +542,8 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
                                 const uint32_t* tiles, const uint32_t* frames, const uint32_t* text,
                                 const uint32_t* off, uint32_t D, const dflop_search_params* sp, dflop_comm* comm,
                                 void* ws, size_t* ws_bytes, dflop_plan_result* out, dflop_cand_result* batch_out,
-                                uint64_t* plan_objective, uint32_t* assign, uint64_t* stage_a_out,
+                                uint64_t* plan_objective, dflop_plan* plans_out, uint32_t* assign,
+                                uint64_t* stage_a_out,
                                 uint64_t stage_a_cap, cudaStream_t s) {
     g_err.clear();
     dflop_status st = validate_cost_model(cm);
@@ -797,6 +798,7 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
             obj += k >> 24;
         }
         if (plan_objective) plan_objective[p] = ok ? obj : ~0ull;
+        if (plans_out) plans_out[p] = plans[p];
         if (ok && obj < best_obj) {
             best_obj = obj;
             win_p = p;
@@ -962,8 +964,8 @@ extern "C" dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_
                                            uint32_t* assign, uint64_t* stage_a_out, uint64_t stage_a_cap,
                                            dflop_stream_t stream) {
     const uint32_t off[2] = {0, n};
-    return search_impl(cl, cm, mm, tiles, frames, text, off, 1, sp, comm, ws, ws_bytes, out, nullptr, nullptr, assign,
-                       stage_a_out, stage_a_cap, (cudaStream_t)stream);
+    return search_impl(cl, cm, mm, tiles, frames, text, off, 1, sp, comm, ws, ws_bytes, out, nullptr, nullptr, nullptr,
+                       assign, stage_a_out, stage_a_cap, (cudaStream_t)stream);
 }
 
 extern "C" dflop_status dflop_search_plans_batches(const dflop_cluster* cl, const dflop_cost_model* cm,
@@ -973,7 +975,7 @@ extern "C" dflop_status dflop_search_plans_batches(const dflop_cluster* cl, cons
                                                    const dflop_search_params* sp, dflop_comm* comm, void* ws,
                                                    size_t* ws_bytes, dflop_plan_result* out,
                                                    dflop_cand_result* batch_results, uint64_t* plan_objective,
-                                                   uint32_t* assign, dflop_stream_t stream) {
+                                                   dflop_plan* plans_out, uint32_t* assign, dflop_stream_t stream) {
     return search_impl(cl, cm, mm, tiles, frames, text, batch_offsets, n_batches, sp, comm, ws, ws_bytes, out,
-                       batch_results, plan_objective, assign, nullptr, 0, (cudaStream_t)stream);
+                       batch_results, plan_objective, plans_out, assign, nullptr, 0, (cudaStream_t)stream);
 }

@@ -498,22 +498,24 @@ def search_plans_batches(model: Dict, tiles, frames, text, batch_offsets: Sequen
     out = PlanResult()
     _check(L.dflop_search_plans_batches(C.byref(cl), C.byref(ms), C.byref(mm), _ptr(tiles), _ptr(frames), _ptr(text),
                                         op, D, C.byref(sp), cptr, None, C.byref(need), C.byref(out), None, None,
-                                        None, None))
+                                        None, None, None))
     wsb = (ws or _default_ws).get(need.value, dev)
     assign = torch.empty(max(n, 1), dtype=torch.int32, device=dev) if want_assign else None
     have = C.c_size_t(wsb.numel())
     bres = (CandResult * D)()
     P = top_p if plan is None else 1
     pobj = np.zeros(P, np.uint64)
+    plans = (Plan * P)()
     _check(L.dflop_search_plans_batches(C.byref(cl), C.byref(ms), C.byref(mm), _ptr(_u32(tiles)), _ptr(_u32(frames)),
                                         _ptr(_u32(text)), op, D, C.byref(sp), cptr, _ptr(wsb), C.byref(have),
-                                        C.byref(out), bres, pobj.ctypes.data_as(C.c_void_p), _ptr(assign),
+                                        C.byref(out), bres, pobj.ctypes.data_as(C.c_void_p), plans, _ptr(assign),
                                         _stream(stream)))
     r = {f: getattr(out, f) for f, _ in PlanResult._fields_ if f not in ("plan", "alg1_plan", "reserved")}
     r["plan"] = out.plan.as_dict()
     r["alg1_plan"] = out.alg1_plan.as_dict()
     r["batches"] = [dict(key=b.key, makespan=b.makespan, cmax=b.cmax, cand=b.cand, status=b.status) for b in bres]
     r["plan_objective"] = pobj
+    r["plans"] = [pl.as_dict() for pl in plans]
     r["assign"] = assign[:n] if assign is not None else None
     return r
 
