@@ -180,7 +180,8 @@ def run_reference(args):
     value = statistics.mean(rates)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-        "warmup": warm, "ms_per_step": 1e3 * K / value, "higher_is_better": True, "scaling": scaling,
+        "warmup": warm, "ms_per_step": 1e3 * K * (p.top_p if p.plan is None else 1) / value,
+        "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "R": p.R, "G": p.G,
                    "note": "reference arm = the CPU oracle (no installable reference: the paper ships no code)"},
