@@ -343,9 +343,10 @@ DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t es, 
 // FIX8: m == 8 * GL and a one-byte assignment (every preset); else any m (loop, bounds).
 template <int GL, bool FIX8>
 DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* apos, uint32_t pa, uint32_t pb,
-                             const ItemRec<uint32_t>& ia, const ItemRec<uint32_t>& ib, uint32_t use, uint32_t jmask,
+                             const ItemRec<uint32_t>& ia, const ItemRec<uint32_t>& ib, uint32_t jmask,
                              uint32_t gl, uint32_t lane, uint32_t m, bool wide) {
-    const uint32_t esa = ia.e & use, lsa = ia.l & use, esb = ib.e & use, lsb = ib.l & use;
+    // never called for c == 0 (its probes use zero items; the single-sample loop does it)
+    const uint32_t esa = ia.e, lsa = ia.l, esb = ib.e, lsb = ib.l;
     uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
     if constexpr (FIX8) {
         // B's two smallest of 8 keys by a merge tree: sorted pairs, then (lo, hi) merges
@@ -421,6 +422,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
     const uint32_t n = p.n, m = p.m, G = p.G;
     const bool wide = p.wide != 0;  // u16 assignment when m > 255
     const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
+    const bool pairs = __all_sync(FULL, c != 0);
     const uint32_t jmask = (1u << sh) - 1u;
     const uint32_t nc = (G - 1 + 3) / 4;  // Philox calls per group
     const uint32_t W = nc ? max(1u, 32u / ((32u / GL) * nc)) : 1u;
@@ -435,14 +437,16 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
         uint32_t t = 0;
 #ifndef DFLOP_NO_LPT_PAIRS
         if constexpr (PK) {
-            // two samples per step (see lpt_pair_step)
-            if (m == 8 * GL && !wide) {
+            // two samples per step (see lpt_pair_step); the warp holding c == 0 takes the
+            // single-sample loop so the pair step needs no probe mask
+            if (!pairs) {
+            } else if (m == 8 * GL && !wide) {
                 for (; t + 1 < ng; t += 2) {
                     const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, true>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.item(pa),
-                                            T.item(pb), (uint32_t)use, jmask, gl, lane, m, false);
+                                            T.item(pb), jmask, gl, lane, m, false);
                 }
             } else {
                 for (; t + 1 < ng; t += 2) {
@@ -450,7 +454,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, false>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                              reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.item(pa),
-                                             T.item(pb), (uint32_t)use, jmask, gl, lane, m, wide);
+                                             T.item(pb), jmask, gl, lane, m, wide);
                 }
             }
         }
