@@ -28,6 +28,8 @@ __global__ void k_init(BalanceHeader* hdr, u64* slot_key, uint32_t n_slots) {
         hdr->sum_e = 0;
         hdr->sum_l = 0;
         hdr->max_key = 0;
+        hdr->max_ld = 0;
+        hdr->offs = 0;
         hdr->variant = 0;
         hdr->shift = 0;
         hdr->status = 0;
@@ -38,7 +40,7 @@ __global__ void k_init(BalanceHeader* hdr, u64* slot_key, uint32_t n_slots) {
 
 // cost rows: ef, eb, lf, lb at cost + r * rs (rs >= n: the row stride)
 __global__ void k_prep_keys(const uint32_t* __restrict__ cost, uint32_t n, size_t rs, BalanceHeader* hdr, u64* keys) {
-    u64 se = 0, sl = 0, mk = 0;
+    u64 se = 0, sl = 0, mk = 0, md = 0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const u64 e = (u64)cost[i] + cost[rs + i];
         const u64 l = (u64)cost[2 * rs + i] + cost[3 * rs + i];
@@ -47,17 +49,21 @@ __global__ void k_prep_keys(const uint32_t* __restrict__ cost, uint32_t n, size_
         se += e;
         sl += l;
         mk = k > mk ? k : mk;
+        md = (l > e && l - e > md) ? l - e : md;
     }
     for (int off = 16; off > 0; off >>= 1) {
         se += __shfl_xor_sync(0xFFFFFFFFu, se, off);
         sl += __shfl_xor_sync(0xFFFFFFFFu, sl, off);
         const u64 o = __shfl_xor_sync(0xFFFFFFFFu, mk, off);
         mk = o > mk ? o : mk;
+        const u64 od = __shfl_xor_sync(0xFFFFFFFFu, md, off);
+        md = od > md ? od : md;
     }
     if ((threadIdx.x & 31) == 0) {
         atomicAdd(&hdr->sum_e, se);
         atomicAdd(&hdr->sum_l, sl);
         atomicMax(&hdr->max_key, mk);
+        atomicMax(&hdr->max_ld, md);
     }
 }
 
@@ -87,10 +93,12 @@ __global__ void k_rank_sort(const u64* __restrict__ keys, uint32_t n, uint32_t* 
 
 // Chooses the candidate-kernel variant and writes the per-position records.
 //   u32 when every bucket sum fits (sums of all e_i, l_i below 2^32 - 1);
-//   packed u32 when every LPT bucket load stays below
-//   2^(32 - s), s = bits of m - 1:
+//   packed u32 when every LPT probe value plus the probe offset C = max_i max(l_i - e_i, 0)
+//   stays below 2^(32 - s), s = bits of m - 1:
 //   a probe's winner has W <= min_j W_j + max(e, l) <= (sum_e + sum_l)/m + max key, every
 //   probe adds at most one more max key, and refinement never raises the maximum (O6).
+//   The candidate kernel probes max(E' + (e' - l' + C'), L' + C') = max(E' + e', L' + l')
+//   - l' + C' (C' = C << s): one fused add-max per bucket, no wrap-around under this bound.
 __global__ void k_build_items(const uint32_t* __restrict__ cost, uint32_t n, size_t rs, uint32_t m, uint32_t allow_pack,
                               BalanceHeader* hdr, const uint32_t* __restrict__ order, ItemRec<uint32_t>* it32,
                               ItemRec<u64>* it64) {
@@ -98,10 +106,11 @@ __global__ void k_build_items(const uint32_t* __restrict__ cost, uint32_t n, siz
     uint32_t sh = 0;
     while ((1u << sh) < m) ++sh;
     const u64 bound = (hdr->sum_e + hdr->sum_l + m - 1) / m + 2 * hdr->max_key;
-    const bool packed = allow_pack && fits && sh < 32 && bound < (1ull << (32 - sh));
+    const bool packed = allow_pack && fits && sh < 32 && bound + hdr->max_ld < (1ull << (32 - sh));
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         hdr->variant = packed ? 0u : (fits ? 1u : 2u);
         hdr->shift = sh;
+        hdr->offs = packed ? (uint32_t)(hdr->max_ld << sh) : 0u;
     }
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const uint32_t i = order[t];
@@ -301,10 +310,6 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) gl = forced;
     cfg.gl = gl;
     const uint32_t per_bucket = (n + m - 1) / std::max(1u, m);
-    uint32_t cap = std::min(128u, std::max(32u, next_pow2(2 * std::max(1u, per_bucket))));
-    const int forced_cap = env_int("DFLOP_CAP", 0);
-    if (forced_cap >= 1 && forced_cap <= 4096) cap = (uint32_t)forced_cap;
-    cfg.cap = cap;
     const bool wide = m > 255;
     cfg.apos_bytes = round16(std::max(16u, n * (wide ? 2u : 1u)));
     // CSR member lists of the refinement: every bucket gets its LPT
@@ -319,15 +324,19 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     // scratch: [cnt, off,] ls[cap], lp[cap] (u16) -- or the 1F1B rings (and, with ORDER4, the
     // ascending / descending slot orders, u16)
     const uint32_t rings = (S + 2 * S * sh.D) * 8u + ((sh.mode & DFLOP_MODE_ORDER4) ? 4u * sh.n_mb : 0u);
-    const uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cfg.cap, rings));
     const size_t smem_max = prop.smem_optin;
     const uint32_t nsm = (uint32_t)prop.sms;
     const uint32_t per_warp = 32u / (uint32_t)gl;  // candidate groups per warp
-    for (int v = 0; v < 3; ++v) {
+    const int forced_cpb = env_int("DFLOP_MAXCPB", 0);  // occupancy experiments
+    struct Lay {
+        uint32_t cb, tbl, cpb;
+        bool tbl_smem;
+    };
+    auto layout = [&](int v, uint32_t cap) {
+        Lay L;
+        const uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cap, rings));
         const uint32_t asz = v == 2 ? 8u : 4u;
         const uint32_t el = round16(m * 2u * asz);   // EL[m] then FL[m]
-        cfg.off_fl[v] = el;
-        cfg.off_scr[v] = 2 * el;
         uint32_t cb = 2 * el + scr;
         // stagger consecutive candidates across banks: a group's probe touches GL*2*asz bytes
         const uint32_t span = std::max(16u, (uint32_t)gl * 2u * asz);
@@ -335,16 +344,47 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
             const uint32_t want = span;  // a multiple of 16 below 128: reachable in <= 7 steps
             while (cb % 128 != want) cb += 16;
         }
-        cfg.cand_bytes[v] = cb;
+        L.cb = cb;
         const uint32_t tbl = (uint32_t)(((size_t)n * (v == 2 ? 32u : 16u) + (size_t)n * 2 + 127) & ~(size_t)127);
         // stage the table in shared memory when it leaves room for at least 2 warps of candidates
-        cfg.tbl_smem[v] = (size_t)tbl + (size_t)2 * per_warp * cb <= smem_max;
-        cfg.tbl_bytes[v] = cfg.tbl_smem[v] ? tbl : 0;
-        uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - cfg.tbl_bytes[v]) / cb, kCandMaxThreads / gl);
+        L.tbl_smem = (size_t)tbl + (size_t)2 * per_warp * cb <= smem_max;
+        L.tbl = L.tbl_smem ? tbl : 0;
+        uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - L.tbl) / cb, kCandMaxThreads / gl);
         // no more groups than the family needs (one CTA per SM), whole warps only
         cpb = std::min<uint32_t>(cpb, std::max(1u, (sh.n_cand + nsm - 1) / nsm));
+        if (forced_cpb >= (int)per_warp) cpb = std::min<uint32_t>(cpb, (uint32_t)forced_cpb);
         cpb = (cpb + per_warp - 1) / per_warp * per_warp;
-        if ((size_t)cfg.tbl_bytes[v] + (size_t)cpb * cb > smem_max) cpb -= per_warp;
+        if ((size_t)L.tbl + (size_t)cpb * cb > smem_max) cpb -= per_warp;
+        L.cpb = cpb;
+        return L;
+    };
+    // shared-memory copies of the first `cap` members of j* and j': about twice the mean list
+    // length, shrunk (not below 32) while that buys resident candidates -- occupancy hides the
+    // latency of the shared-memory and shuffle chains (config 5: cap 128 -> 96 raises 72 -> 80
+    // candidates per SM, -6.7%; 768-thread blocks would need <= 80 registers: +37%)
+    uint32_t cap = std::min(128u, std::max(32u, next_pow2(2 * std::max(1u, per_bucket))));
+    {
+        uint32_t best = cap, best_cpb = layout(0, cap).cpb;
+        for (uint32_t c2 = cap - 8; c2 >= 32 && c2 < cap; c2 -= 8) {
+            const uint32_t q = layout(0, c2).cpb;
+            if (q > best_cpb) {
+                best_cpb = q;
+                best = c2;
+            }
+        }
+        cap = best;
+    }
+    const int forced_cap = env_int("DFLOP_CAP", 0);
+    if (forced_cap >= 1 && forced_cap <= 4096) cap = (uint32_t)forced_cap;
+    cfg.cap = cap;
+    for (int v = 0; v < 3; ++v) {
+        const Lay L = layout(v, cap);
+        const uint32_t cb = L.cb, cpb = L.cpb;
+        cfg.cand_bytes[v] = cb;
+        cfg.tbl_smem[v] = L.tbl_smem;
+        cfg.tbl_bytes[v] = L.tbl;
+        cfg.off_fl[v] = round16(m * 2u * (v == 2 ? 8u : 4u));
+        cfg.off_scr[v] = 2 * cfg.off_fl[v];
         if (cpb == 0) {
             char buf[200];
             snprintf(buf, sizeof buf,

@@ -12,7 +12,10 @@ namespace dflop {
 constexpr int kVariants = 3;
 // block size cap of the candidate kernel: leaves ~100 registers per thread (64 K per SM);
 // the 1024-thread bound capped the kernel at 64 registers and cost ~10%
-constexpr int kCandMaxThreads = 640;
+#ifndef DFLOP_CAND_MAX_THREADS
+#define DFLOP_CAND_MAX_THREADS 640
+#endif
+constexpr int kCandMaxThreads = DFLOP_CAND_MAX_THREADS;
 
 // Per-launch parameters.  Shared-memory layout (bytes):
 //   [0, tbl_bytes)              CTA item table: ItemRec<A>[n] then u16 pos->item[n]

@@ -284,15 +284,28 @@ DFLOP_DEV void each_entry(const uint4 v, uint32_t blk, bool wide, uint32_t m, F&
 // CSR member lists of all m buckets from the assignment: cnt[j] members of bucket j at
 // csr[off[j] ..], off[j+1] - off[j] = (LPT count) + sigma.  Two 16-byte L2 passes (count,
 // then scatter); the list order is irrelevant (the pair search is a keyed minimum).
-template <int GL>
-DFLOP_DEV void build_lists(const CandParams& p, const uint8_t* apos, bool wide, uint32_t* cnt, uint32_t* off,
-                           uint16_t* csr, uint32_t gl) {
+// With FL != null (the first build after LPT) the count pass also forms the forward sums
+// FL[j] = (sum EF, sum LF) of the members (shared-memory atomics): the LPT steps then update
+// only EL -- one atomic per 8 entries of a warp instead of a read-modify-write per sample.
+template <typename A, int GL, bool SM>
+DFLOP_DEV void build_lists(const CandParams& p, const Tbl<A, SM>& T, const uint8_t* apos, bool wide, uint32_t* cnt,
+                           uint32_t* off, uint16_t* csr, uint32_t gl, Pair2<A>* FL) {
     const uint32_t m = p.m, nblk = p.apos_bytes / 16, sig = p.sigma;
     const uint4* ap = reinterpret_cast<const uint4*>(apos);
     for (uint32_t j = gl; j < m; j += GL) cnt[j] = 0;
     __syncwarp(FULL);
-    for (uint32_t b = gl; b < nblk; b += GL)
-        each_entry(__ldcg(ap + b), b, wide, m, [&](uint32_t, uint32_t j) { atomicAdd(&cnt[j], 1u); });
+    if (FL) {
+        for (uint32_t b = gl; b < nblk; b += GL)
+            each_entry(__ldcg(ap + b), b, wide, m, [&](uint32_t pos, uint32_t j) {
+                atomicAdd(&cnt[j], 1u);
+                const ItemRec<A> r = T.item(pos);
+                atomicAdd(&FL[j].a, r.ef);
+                atomicAdd(&FL[j].b, r.lf);
+            });
+    } else {
+        for (uint32_t b = gl; b < nblk; b += GL)
+            each_entry(__ldcg(ap + b), b, wide, m, [&](uint32_t, uint32_t j) { atomicAdd(&cnt[j], 1u); });
+    }
     __syncwarp(FULL);
     // exclusive prefix of cnt[j] + sigma, GL buckets per step (coalesced when the counters
     // live in global memory); counters reset for the scatter pass
@@ -322,15 +335,31 @@ DFLOP_DEV void build_lists(const CandParams& p, const uint8_t* apos, bool wide, 
     __syncwarp(FULL);
 }
 
-// Q buckets per lane (m == Q*GL), fully unrolled: two running minima of the packed keys
+// FL[j] = (sum EF, sum LF) over the members of bucket j, from the assignment (when no
+// refinement round runs: m == 1 or R == 0; otherwise the first build_lists forms it)
+template <typename A, int GL, bool SM>
+DFLOP_DEV void form_fl(const CandParams& p, const Tbl<A, SM>& T, const uint8_t* apos, bool wide, Pair2<A>* FL,
+                       uint32_t gl) {
+    const uint4* ap = reinterpret_cast<const uint4*>(apos);
+    for (uint32_t b = gl; b < p.apos_bytes / 16; b += GL)
+        each_entry(__ldcg(ap + b), b, wide, p.m, [&](uint32_t pos, uint32_t j) {
+            const ItemRec<A> r = T.item(pos);
+            atomicAdd(&FL[j].a, r.ef);
+            atomicAdd(&FL[j].b, r.lf);
+        });
+    __syncwarp(FULL);
+}
+
+// Q buckets per lane (m == Q*GL), fully unrolled: two running minima of the packed keys.
+// The packed buckets hold (E', L' + C') and d = e' - l' + C' (see lpt_pass): one fused add-max
+// per probe, max(E' + d, L' + C') = max(E' + e', L' + l') - l' + C'.
 template <int Q, int GL>
-DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t es, uint32_t ls, uint32_t& b0,
-                           uint32_t& b1) {
+DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t d, uint32_t& b0, uint32_t& b1) {
 #pragma unroll
     for (uint32_t k = 0; k < Q; k += 2) {
         const Pair2<uint32_t> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
-        b0 = min(b0, max(x.a + es, x.b + ls));
-        b1 = min(b1, max(y.a + es, y.b + ls));
+        b0 = min(b0, max(x.a + d, x.b));
+        b1 = min(b1, max(y.a + d, y.b));
     }
 }
 
@@ -344,9 +373,9 @@ DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t es, 
 template <int GL, bool FIX8>
 DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* apos, uint32_t pa, uint32_t pb,
                              const ItemRec<uint32_t>& ia, const ItemRec<uint32_t>& ib, uint32_t jmask,
-                             uint32_t gl, uint32_t lane, uint32_t m, bool wide) {
+                             uint32_t gl, uint32_t lane, uint32_t m, bool wide, uint32_t co) {
     // never called for c == 0 (its probes use zero items; the single-sample loop does it)
-    const uint32_t esa = ia.e, lsa = ia.l, esb = ib.e, lsb = ib.l;
+    const uint32_t da = ia.e - ia.l + co, db = ib.e - ib.l + co;  // probe offsets (lpt_pass)
     uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
     if constexpr (FIX8) {
         // B's two smallest of 8 keys by a merge tree: sorted pairs, then (lo, hi) merges
@@ -355,9 +384,9 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
 #pragma unroll
         for (uint32_t k = 0; k < 8; k += 2) {
             const Pair2<uint32_t> x = EL[gl + GL * k], y = EL[gl + GL * (k + 1)];
-            a0 = min(a0, max(x.a + esa, x.b + lsa));
-            a1 = min(a1, max(y.a + esa, y.b + lsa));
-            const uint32_t vx = max(x.a + esb, x.b + lsb), vy = max(y.a + esb, y.b + lsb);
+            a0 = min(a0, max(x.a + da, x.b));
+            a1 = min(a1, max(y.a + da, y.b));
+            const uint32_t vx = max(x.a + db, x.b), vy = max(y.a + db, y.b);
             lo[k / 2] = min(vx, vy);
             hi[k / 2] = max(vx, vy);
         }
@@ -369,8 +398,8 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
 #pragma unroll 2
         for (uint32_t j = gl; j < m; j += GL) {
             const Pair2<uint32_t> x = EL[j];
-            a0 = min(a0, max(x.a + esa, x.b + lsa));
-            const uint32_t vx = max(x.a + esb, x.b + lsb);
+            a0 = min(a0, max(x.a + da, x.b));
+            const uint32_t vx = max(x.a + db, x.b);
             m2 = min(m2, max(m1, vx));
             m1 = min(m1, vx);
         }
@@ -389,23 +418,20 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
     uint32_t alt = 0xFFFFFFFFu;
     if (own_a) {
         ela = EL[ja];
-        alt = min(m2, max(ela.a + ia.e + esb, ela.b + ia.l + lsb));  // a* after A, probed by B
+        alt = min(m2, max(ela.a + ia.e + db, ela.b + ia.l));  // a* after A, probed by B
     }
     alt = __shfl_sync(FULL, alt, (lane & ~(uint32_t)(GL - 1)) | (ja & (GL - 1)));
     const uint32_t jb = (((m1 & jmask) != ja) ? m1 : alt) & jmask;
     if (own_a) {
-        EL[ja] = Pair2<uint32_t>{ela.a + ia.e, ela.b + ia.l};
-        Pair2<uint32_t> fl = FL[ja];
-        FL[ja] = Pair2<uint32_t>{fl.a + ia.ef, fl.b + ia.lf};
+        EL[ja] = Pair2<uint32_t>{ela.a + ia.e, ela.b + ia.l};  // FL: formed by the first build_lists
         if constexpr (FIX8)
             apos[pa] = (uint8_t)ja;
         else
             set_apos(apos, pa, ja, wide);
     }
     if ((jb & (GL - 1)) == gl) {  // after A's update in program order when jb = ja (same lane)
-        const Pair2<uint32_t> el = EL[jb], fl = FL[jb];
+        const Pair2<uint32_t> el = EL[jb];
         EL[jb] = Pair2<uint32_t>{el.a + ib.e, el.b + ib.l};
-        FL[jb] = Pair2<uint32_t>{fl.a + ib.ef, fl.b + ib.lf};
         if constexpr (FIX8)
             apos[pb] = (uint8_t)jb;
         else
@@ -416,9 +442,14 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
 // ---------------------------------------------------------------- LPT pass (R12)
 // c == 0: argmin of the current max(E_j, L_j) (the paper's rule); c >= 1: argmin of the
 // resulting max(E_j + e_i, L_j + l_i); lowest j on ties.
+// Packed variant: during this pass bucket j holds (E_j << s | j, (L_j << s | j) + co) with
+// co = C << s, C = max_i max(l_i - e_i, 0) (k_build_items), and a sample probes with
+// d = e' - l' + co >= 0: max(E' + d, L' + co) = max(E' + e', L' + l') - l' + co, the same
+// order over j (and the index bits) as the resulting max, without wrap-around (the variant's
+// bound covers probe + C); c == 0 probes with d = co.
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
-                        Pair2<A>* FL, uint8_t* apos, uint32_t gl) {
+                        Pair2<A>* FL, uint8_t* apos, uint32_t gl, uint32_t co) {
     const uint32_t n = p.n, m = p.m, G = p.G;
     const bool wide = p.wide != 0;  // u16 assignment when m > 255
     const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
@@ -446,7 +477,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, true>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.item(pa),
-                                            T.item(pb), jmask, gl, lane, m, false);
+                                            T.item(pb), jmask, gl, lane, m, false, co);
                 }
             } else {
                 for (; t + 1 < ng; t += 2) {
@@ -454,7 +485,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, false>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                              reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.item(pa),
-                                             T.item(pb), jmask, gl, lane, m, wide);
+                                             T.item(pb), jmask, gl, lane, m, wide, co);
                 }
             }
         }
@@ -465,25 +496,25 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
             uint32_t bj;
             if (PK) {
                 // keys (W << s) | j: one fused add-max and one min per probe
-                const uint32_t es = (uint32_t)it.e & (uint32_t)use, ls = (uint32_t)it.l & (uint32_t)use;
+                const uint32_t d = (((uint32_t)it.e - (uint32_t)it.l) & (uint32_t)use) + co;
                 uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
                 if (m == 8 * GL) {  // every preset: exactly 8 buckets per lane, no bounds tests
-                    probe_fixed<8, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, es, ls, b0, b1);
+                    probe_fixed<8, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, d, b0, b1);
                 } else if (m == 16 * GL) {
-                    probe_fixed<16, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, es, ls, b0, b1);
+                    probe_fixed<16, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, d, b0, b1);
                 } else if (m == 32 * GL) {
-                    probe_fixed<32, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, es, ls, b0, b1);
+                    probe_fixed<32, GL>(reinterpret_cast<const Pair2<uint32_t>*>(EL), gl, d, b0, b1);
                 } else if (m < 8 * GL) {  // at most 8 buckets per lane, fully unrolled
 #pragma unroll
                     for (uint32_t k = 0; k < 8; k += 2) {
                         const uint32_t j0 = gl + GL * k, j1 = j0 + GL;
                         if (j0 < m) {
                             const Pair2<A> x = EL[j0];
-                            b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                            b0 = min(b0, max((uint32_t)x.a + d, (uint32_t)x.b));
                         }
                         if (j1 < m) {
                             const Pair2<A> y = EL[j1];
-                            b1 = min(b1, max((uint32_t)y.a + es, (uint32_t)y.b + ls));
+                            b1 = min(b1, max((uint32_t)y.a + d, (uint32_t)y.b));
                         }
                     }
                 } else {
@@ -491,12 +522,12 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
 #pragma unroll 4
                     for (; j + GL < m; j += 2 * GL) {
                         const Pair2<A> x = EL[j], y = EL[j + GL];
-                        b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
-                        b1 = min(b1, max((uint32_t)y.a + es, (uint32_t)y.b + ls));
+                        b0 = min(b0, max((uint32_t)x.a + d, (uint32_t)x.b));
+                        b1 = min(b1, max((uint32_t)y.a + d, (uint32_t)y.b));
                     }
                     if (j < m) {
                         const Pair2<A> x = EL[j];
-                        b0 = min(b0, max((uint32_t)x.a + es, (uint32_t)x.b + ls));
+                        b0 = min(b0, max((uint32_t)x.a + d, (uint32_t)x.b));
                     }
                 }
                 uint32_t best = min(b0, b1);
@@ -521,13 +552,10 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
             // during LPT bucket j is read and written only by its owner lane j % GL, so the
             // update needs no warp barrier (the shuffles already order the lanes)
             if ((bj & (GL - 1)) == gl) {
-                Pair2<A> el = EL[bj], fl = FL[bj];
+                Pair2<A> el = EL[bj];
                 el.a += it.e;
                 el.b += it.l;
-                fl.a += it.ef;
-                fl.b += it.lf;
-                EL[bj] = el;
-                FL[bj] = fl;
+                EL[bj] = el;  // FL: formed by the first build_lists (or fl_sums for m == 1)
                 set_apos(apos, pos, bj, wide);
             }
         }
@@ -560,10 +588,12 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
     uint32_t* off = cnt + m;
     uint16_t* lp = ls + cap;
     bool dirty = true;  // the lists must be (re)built from the assignment
+    bool first = true;  // the first build also forms FL (LPT maintains EL only)
     for (uint32_t r = 0; r < p.R; ++r) {
         if (__any_sync(FULL, dirty)) {  // warp-uniform: a clean group rebuilds the same lists
-            build_lists<GL>(p, apos, wide, cnt, off, csr, gl);
+            build_lists<A, GL, SM>(p, T, apos, wide, cnt, off, csr, gl, first ? FL : nullptr);
             dirty = false;
+            first = false;
         }
         // bottleneck bucket j* = lowest j with maximal W_j = max(E_j, L_j)
         A Wb = 0;
@@ -854,12 +884,12 @@ DFLOP_DEV u64 score_order4(const CandParams& p, uint32_t sh, const Pair2<A>* EL,
 }
 
 template <typename A, bool PK, int GL, bool SM, bool O4>
-DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
+DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, uint32_t co, Pair2<A>* EL,
                              Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, u64& Tc,
                              u64& cmax, PhaseTimer& ph) {
     const uint32_t m = p.m;
     for (uint32_t j = gl; j < m; j += GL) {
-        EL[j] = PK ? Pair2<A>{(A)j, (A)j} : Pair2<A>{0, 0};
+        EL[j] = PK ? Pair2<A>{(A)j, (A)(j + co)} : Pair2<A>{0, 0};  // co: the LPT probe offset
         FL[j] = Pair2<A>{0, 0};
     }
     __syncwarp(FULL);
@@ -881,9 +911,16 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         }
         __syncwarp(FULL);
     } else {
-        lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, gl);
+        lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, gl, co);
+        if (PK) {  // drop the probe offset: plain packed keys from here on
+            for (uint32_t j = gl; j < m; j += GL) EL[j].b -= (A)co;
+            __syncwarp(FULL);
+        }
         ph.mark(0);
-        if (m >= 2) refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
+        if (m >= 2 && p.R > 0)
+            refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
+        else
+            form_fl<A, GL, SM>(p, T, apos, p.wide != 0, FL, gl);
     }
     A cm = 0;
     for (uint32_t j = gl; j < m; j += GL) {
@@ -903,6 +940,7 @@ template <typename A, bool PK, int GL, bool SM, bool O4>
 __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     if (p.hdr->variant != p.want_variant) return;  // another variant runs
     const uint32_t sh = PK ? p.hdr->shift : 0u;
+    const uint32_t co = PK ? p.hdr->offs : 0u;  // LPT probe offset (lpt_pass)
     extern __shared__ __align__(128) uint8_t smem[];
     Tbl<A, SM> T;
     if (SM) {
@@ -945,7 +983,7 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         const uint32_t c = valid ? c0 + grp : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
         u64 Tc, cmax;
-        run_candidate<A, PK, GL, SM, O4>(p, T, c, sh, EL, FL, apos, scr, csr, gl, Tc, cmax, ph);
+        run_candidate<A, PK, GL, SM, O4>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
         u64 key;
         if (Tc >= (1ull << 40)) {

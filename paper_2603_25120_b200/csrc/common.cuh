@@ -68,6 +68,8 @@ struct BalanceHeader {
     uint32_t variant;       // candidate kernel variant: 0 packed u32, 1 plain u32, 2 u64
     uint32_t shift;         // bucket-index bits of the packed variant
     uint32_t status;        // DFLOP_DEV_* bits
-    uint32_t pad[25];
+    uint32_t offs;          // packed variant: C << shift, C = max_ld (the LPT probe offset)
+    u64 max_ld;             // max_i max(l_i - e_i, 0)
+    uint32_t pad[22];
 };
 static_assert(sizeof(BalanceHeader) == 144, "header layout");
