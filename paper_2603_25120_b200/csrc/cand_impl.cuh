@@ -207,6 +207,12 @@ DFLOP_DEV uint64_t batch_perms(uint32_t g0, uint32_t W, uint32_t nc, uint32_t c,
     return perm;
 }
 
+// Pair score max(se + a, sl + b, pe - a, pl - b) of moving i (row) to j' and i' (a, b) to j*
+// (O6), 32-bit: one subtraction and three fused add-max instructions
+DFLOP_DEV uint32_t score4(uint32_t se, uint32_t sl, uint32_t pe, uint32_t pl, uint32_t a, uint32_t b) {
+    return __viaddmax_u32(se, a, __viaddmax_u32(sl, b, __viaddmax_u32(pe, 0u - a, pl - b)));
+}
+
 // (hi << 32 | lo) as a register pair, without 64-bit arithmetic
 DFLOP_DEV u64 pack64(uint32_t hi, uint32_t lo) {
     u64 r;
@@ -414,13 +420,10 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
     }
     const uint32_t ja = ba & jmask;
     const bool own_a = (ja & (GL - 1)) == gl;
-    Pair2<uint32_t> ela{0, 0};
-    uint32_t alt = 0xFFFFFFFFu;
-    if (own_a) {
-        ela = EL[ja];
-        alt = min(m2, max(ela.a + ia.e + db, ela.b + ia.l));  // a* after A, probed by B
-    }
-    alt = __shfl_sync(FULL, alt, (lane & ~(uint32_t)(GL - 1)) | (ja & (GL - 1)));
+    // every lane of the group reads a* (one broadcast load) and evaluates B's probe of a*
+    // after A itself -- no shuffle from the owner on the dependency chain
+    const Pair2<uint32_t> ela = EL[ja];
+    const uint32_t alt = min(m2, max(ela.a + ia.e + db, ela.b + ia.l));  // a* after A, probed by B
     const uint32_t jb = (((m1 & jmask) != ja) ? m1 : alt) & jmask;
     if (own_a) {
         EL[ja] = Pair2<uint32_t>{ela.a + ia.e, ela.b + ia.l};  // FL: formed by the first build_lists
@@ -598,15 +601,30 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         // bottleneck bucket j* = lowest j with maximal W_j = max(E_j, L_j)
         A Wb = 0;
         uint32_t jb = 0xFFFFFFFFu;
-        for (uint32_t j = gl; j < m; j += GL) {
-            const Pair2<A> el = EL[j];
-            const A W = keyval<A, PK>(maxa(el.a, el.b), sh);
-            if (jb == 0xFFFFFFFFu || W > Wb) {
-                Wb = W;
-                jb = j;
+        if constexpr (PK) {
+            // packed keys: (W << s) | (jmask - j) -- one max per bucket and per reduction
+            // round gives the largest W and, among equal W, the lowest j
+            const uint32_t jmask = (1u << sh) - 1u;
+            uint32_t kb = 0;
+            for (uint32_t j = gl; j < m; j += GL) {
+                const Pair2<A> el = EL[j];
+                kb = max(kb, (uint32_t)keyval<A, PK>(maxa(el.a, el.b), sh) | (jmask - j));
             }
+#pragma unroll
+            for (int o = GL / 2; o > 0; o >>= 1) kb = max(kb, __shfl_xor_sync(FULL, kb, o));
+            Wb = (A)(kb & ~jmask);
+            jb = jmask - (kb & jmask);
+        } else {
+            for (uint32_t j = gl; j < m; j += GL) {
+                const Pair2<A> el = EL[j];
+                const A W = keyval<A, PK>(maxa(el.a, el.b), sh);
+                if (jb == 0xFFFFFFFFu || W > Wb) {
+                    Wb = W;
+                    jb = j;
+                }
+            }
+            argmax_reduce<A, GL>(Wb, jb, FULL);
         }
-        argmax_reduce<A, GL>(Wb, jb, FULL);
         const uint32_t js = jb;
         const A Ws = Wb;
         const Philox4 w = philox4x32_10(r, c, 1u, 0u, p.seed0, p.seed1);
@@ -665,12 +683,16 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             }
             auto pair = [&](uint32_t pj) {
                 const Pair2<A> b = T.el(pj);
-                const A s0 = maxa(maxa<A>(se0 + b.a, sl0 + b.b), maxa<A>(pe0 - b.a, pl0 - b.b));
-                const A s1 = maxa(maxa<A>(se1 + b.a, sl1 + b.b), maxa<A>(pe1 - b.a, pl1 - b.b));
                 if (sizeof(A) == 4) {
-                    r0 = min(r0, (uint32_t)s0);
-                    r1 = min(r1, (uint32_t)s1);
+                    // the same four-term maximum as one chain of fused add-max (DPX): every
+                    // term is a non-negative load below 2^32, so the wrapping -b.a is exact
+                    r0 = min(r0, score4((uint32_t)se0, (uint32_t)sl0, (uint32_t)pe0, (uint32_t)pl0, (uint32_t)b.a,
+                                        (uint32_t)b.b));
+                    r1 = min(r1, score4((uint32_t)se1, (uint32_t)sl1, (uint32_t)pe1, (uint32_t)pl1, (uint32_t)b.a,
+                                        (uint32_t)b.b));
                 } else {
+                    const A s0 = maxa(maxa<A>(se0 + b.a, sl0 + b.b), maxa<A>(pe0 - b.a, pl0 - b.b));
+                    const A s1 = maxa(maxa<A>(se1 + b.a, sl1 + b.b), maxa<A>(pe1 - b.a, pl1 - b.b));
                     const uint32_t rk = T.idx(pj) + 1u;
                     lex_update(bsc, bi, brk, s0, i0, rk);
                     lex_update(bsc, bi, brk, s1, i1, rk);

@@ -179,6 +179,33 @@ def test_balance_edge_cases(D, O, case):
         check_balance(D, O, q, plan, K=300, R=6, G=G, seed=(n, 3), c0=0, c1=40)
 
 
+def _packed_margin(q, m):
+    """bound + C of the packed variant (k_build_items): ceil((sum e + sum l)/m) + 2 max key + max(l - e)+"""
+    q = q.astype(np.int64)
+    e, l = q[0] + q[1], q[2] + q[3]
+    return -(-(int(e.sum()) + int(l.sum())) // m) + 2 * int(np.maximum(e, l).max()) + int(np.maximum(l - e, 0).max())
+
+
+@pytest.mark.parametrize("side", [-1, 0, 1])
+def test_balance_packed_offset_bound(D, O, side):
+    # one LLM-heavy item (e = 0) sets C = max(l - e) and the max key; its size puts the packed
+    # variant's bound + C just below / at / above 2^(32 - s): the LPT probes in the offset form
+    # max(E' + e' - l' + C', L' + C') reach the top of the u32 range, or the plain u32 variant runs
+    plan = dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=3, l_dp=1, n_mb=16)
+    m, s = 16, 4
+    q = synth.random_costs(200, seed=5, hi=200000)
+    lim = 1 << (32 - s)
+    lo, hi = 0, lim
+    while hi - lo > 1:  # largest LLM size X of item 0 with margin < lim
+        X = (lo + hi) // 2
+        q[:, 0] = (0, 0, X // 3, X - X // 3)
+        lo, hi = (X, hi) if _packed_margin(q, m) < lim else (lo, X)
+    X = lo + (1 if side > 0 else 0) - (5 if side < 0 else 0)
+    q[:, 0] = (0, 0, X // 3, X - X // 3)
+    assert (_packed_margin(q, m) < lim) == (side <= 0)
+    check_balance(D, O, q, plan, K=512, R=8, G=8, seed=(9, side + 1), c0=0, c1=512)
+
+
 def test_balance_64bit_path(D, O, presets):
     # 1 ns ticks: config 2's bucket sums exceed 2^32 -> 64-bit candidate kernel
     p = presets[2]
