@@ -378,10 +378,10 @@ DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t d, u
 // FIX8: m == 8 * GL and a one-byte assignment (every preset); else any m (loop, bounds).
 template <int GL, bool FIX8>
 DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* apos, uint32_t pa, uint32_t pb,
-                             const ItemRec<uint32_t>& ia, const ItemRec<uint32_t>& ib, uint32_t jmask,
+                             const Pair2<uint32_t> ia, const Pair2<uint32_t> ib, uint32_t jmask,
                              uint32_t gl, uint32_t lane, uint32_t m, bool wide, uint32_t co) {
     // never called for c == 0 (its probes use zero items; the single-sample loop does it)
-    const uint32_t da = ia.e - ia.l + co, db = ib.e - ib.l + co;  // probe offsets (lpt_pass)
+    const uint32_t da = ia.a - ia.b + co, db = ib.a - ib.b + co;  // probe offsets (lpt_pass)
     uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
     if constexpr (FIX8) {
         // B's two smallest of 8 keys by a merge tree: sorted pairs, then (lo, hi) merges
@@ -423,10 +423,10 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
     // every lane of the group reads a* (one broadcast load) and evaluates B's probe of a*
     // after A itself -- no shuffle from the owner on the dependency chain
     const Pair2<uint32_t> ela = EL[ja];
-    const uint32_t alt = min(m2, max(ela.a + ia.e + db, ela.b + ia.l));  // a* after A, probed by B
+    const uint32_t alt = min(m2, max(ela.a + ia.a + db, ela.b + ia.b));  // a* after A, probed by B
     const uint32_t jb = (((m1 & jmask) != ja) ? m1 : alt) & jmask;
     if (own_a) {
-        EL[ja] = Pair2<uint32_t>{ela.a + ia.e, ela.b + ia.l};  // FL: formed by the first build_lists
+        EL[ja] = Pair2<uint32_t>{ela.a + ia.a, ela.b + ia.b};  // FL: formed by the first build_lists
         if constexpr (FIX8)
             apos[pa] = (uint8_t)ja;
         else
@@ -434,7 +434,7 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
     }
     if ((jb & (GL - 1)) == gl) {  // after A's update in program order when jb = ja (same lane)
         const Pair2<uint32_t> el = EL[jb];
-        EL[jb] = Pair2<uint32_t>{el.a + ib.e, el.b + ib.l};
+        EL[jb] = Pair2<uint32_t>{el.a + ib.a, el.b + ib.b};
         if constexpr (FIX8)
             apos[pb] = (uint8_t)jb;
         else
@@ -479,23 +479,24 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, true>(reinterpret_cast<Pair2<uint32_t>*>(EL),
-                                            reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.item(pa),
-                                            T.item(pb), jmask, gl, lane, m, false, co);
+                                            reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
+                                            T.el(pb), jmask, gl, lane, m, false, co);
                 }
             } else {
                 for (; t + 1 < ng; t += 2) {
                     const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, false>(reinterpret_cast<Pair2<uint32_t>*>(EL),
-                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.item(pa),
-                                             T.item(pb), jmask, gl, lane, m, wide, co);
+                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
+                                             T.el(pb), jmask, gl, lane, m, wide, co);
                 }
             }
         }
 #endif
         for (; t < ng; ++t) {
             const uint32_t pos = start + (uint32_t)((perm >> (4 * t)) & 15ull);
-            const ItemRec<A> it = T.item(pos);
+            const Pair2<A> el2 = T.el(pos);  // (e, l): 8-byte loads (the sample's record half)
+            const ItemRec<A> it{el2.a, el2.b, 0, 0};
             uint32_t bj;
             if (PK) {
                 // keys (W << s) | j: one fused add-max and one min per probe
