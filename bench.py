@@ -342,6 +342,9 @@ def main():
             if "ncu_issue_active" in tr:
                 roofline["ncu_issue_active"] = tr["ncu_issue_active"]
                 roofline["ncu_threads_per_warp_instruction"] = tr.get("ncu_threads_per_warp_instruction")
+                for k in ("ncu_lsu_data_pipe_wavefronts", "ncu_alu_pipe"):  # the two busiest pipes
+                    if k in tr:
+                        roofline[k] = tr[k]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
