@@ -379,7 +379,7 @@ DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t d, u
 template <int GL, bool FIX8>
 DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* apos, uint32_t pa, uint32_t pb,
                              const Pair2<uint32_t> ia, const Pair2<uint32_t> ib, uint32_t jmask,
-                             uint32_t gl, uint32_t lane, uint32_t m, bool wide, uint32_t co) {
+                             uint32_t gl, uint32_t m, bool wide, uint32_t co) {
     // never called for c == 0 (its probes use zero items; the single-sample loop does it)
     const uint32_t da = ia.a - ia.b + co, db = ib.a - ib.b + co;  // probe offsets (lpt_pass)
     uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
@@ -480,7 +480,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, true>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
-                                            T.el(pb), jmask, gl, lane, m, false, co);
+                                            T.el(pb), jmask, gl, m, false, co);
                 }
             } else {
                 for (; t + 1 < ng; t += 2) {
@@ -488,7 +488,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, false>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                              reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
-                                             T.el(pb), jmask, gl, lane, m, wide, co);
+                                             T.el(pb), jmask, gl, m, wide, co);
                 }
             }
         }
