@@ -189,12 +189,33 @@ def run_reference(args):
                          "sample": f"each step: {sample}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
+
+
+# The JSON line is the only thing this program writes to stdout: file descriptor 1 is pointed
+# at stderr for everything else (NCCL prints its version banner to stdout when NCCL_DEBUG is
+# set, and other C libraries may print too); emit() writes to the saved original stdout.
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    _claim_stdout()
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
 
 
 # ---------------------------------------------------------------- the GPU arm
 def main():
+    _claim_stdout()
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -367,7 +388,7 @@ def main():
         v, sample, thr = oracle_rate(p, K, args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if comm is not None:
         comm.close()
     if world > 1:

@@ -1001,9 +1001,15 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     u64 best_key = ~0ull, best_T = 0, best_cmax = 0;
     PhaseTimer ph;
     ph.start(p.phase);
-    for (uint32_t c0 = p.c_begin + blockIdx.x * cpb; c0 < p.c_end; c0 += gridDim.x * cpb) {
-        const bool valid = c0 + grp < p.c_end;
-        const uint32_t c = valid ? c0 + grp : p.c_end - 1;  // tail groups recompute a real candidate
+    // a full round hands candidates base + block * cpb + grp to the block's groups; a partial
+    // last round hands base + grp * grid + block, so its candidates are spread over every SM
+    // (a few warps each, at low contention) instead of filling a few SMs
+    const uint32_t stride = gridDim.x * cpb;
+    for (uint32_t base = p.c_begin; base < p.c_end; base += stride) {
+        const uint32_t cc = base + (p.c_end - base >= stride ? blockIdx.x * cpb + grp : grp * gridDim.x + blockIdx.x);
+        const bool valid = cc < p.c_end;
+        if (!__any_sync(FULL, valid)) break;  // warp-uniform: every group of the warp is done
+        const uint32_t c = valid ? cc : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
         u64 Tc, cmax;
         run_candidate<A, PK, GL, SM, O4>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph);
