@@ -729,6 +729,16 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
                 set_error("internal: balance workspace %zu > bound %zu", bpn.cfg.total, L.bal_bytes);
                 return DFLOP_ERR_UNSUPPORTED;
             }
+            if (ns > 1) {
+                // concurrent plans: the fewest blocks that keep the number of rounds minimal,
+                // so the last round is nearly full and the SMs left over run the next plan
+                // (a single launch keeps every SM and spreads a partial last round instead)
+                for (int v = 0; v < 3; ++v) {
+                    const uint32_t cpb = std::max(1u, bpn.cfg.cpb[v]), g = std::max(1u, bpn.cfg.grid[v]);
+                    const uint32_t want = (cend - cb + cpb - 1) / cpb, rounds = std::max(1u, (want + g - 1) / g);
+                    bpn.cfg.grid[v] = std::max(1u, std::min(g, (want + rounds - 1) / rounds));
+                }
+            }
             BalanceArgs a{};
             a.cost_ticks = costs + (size_t)p * pstride + o;
             a.cost_stride = n_tot;
