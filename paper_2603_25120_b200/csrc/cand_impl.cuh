@@ -457,7 +457,10 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
     const bool wide = p.wide != 0;  // u16 assignment when m > 255
     const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
     const bool pairs = __all_sync(FULL, c != 0);
-    const uint32_t jmask = (1u << sh) - 1u;
+    const uint32_t jmask = PK ? (1u << sh) - 1u : 0u;
+    // plain 32-bit variant with lane-local packed LPT keys (k_candidates): sh = 0x100 | kb
+    const uint32_t ush = (!PK && sizeof(A) == 4 && sh >= 0x100u) ? (sh & 0xFFu) : 0u;
+    const bool lanepk = !PK && sizeof(A) == 4 && sh >= 0x100u;
     const uint32_t nc = (G - 1 + 3) / 4;  // Philox calls per group
     const uint32_t W = nc ? max(1u, 32u / ((32u / GL) * nc)) : 1u;
     const uint32_t lane = threadIdx.x & 31u, mycg = lane / GL;
@@ -538,6 +541,30 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
 #pragma unroll
                 for (int off = GL / 2; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(FULL, best, off));
                 bj = best & jmask;
+            } else if (lanepk) {
+                // lane-local keys (v << kb | k) for bucket j = gl + GL*k: one fused add-max per
+                // bucket as in the packed variant; the key minimum orders (v, k), and a tie of
+                // (v, k) across lanes goes to the lowest lane (ballot) -- the lowest j
+                const uint32_t d = ((((uint32_t)it.e - (uint32_t)it.l) << ush) & (uint32_t)use) + co;
+                uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
+                uint32_t j = gl;
+#pragma unroll 4
+                for (; j + GL < m; j += 2 * GL) {
+                    const Pair2<A> x = EL[j], y = EL[j + GL];
+                    b0 = min(b0, max((uint32_t)x.a + d, (uint32_t)x.b));
+                    b1 = min(b1, max((uint32_t)y.a + d, (uint32_t)y.b));
+                }
+                if (j < m) {
+                    const Pair2<A> x = EL[j];
+                    b0 = min(b0, max((uint32_t)x.a + d, (uint32_t)x.b));
+                }
+                const uint32_t mine = min(b0, b1);
+                uint32_t best = mine;
+#pragma unroll
+                for (int off = GL / 2; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(FULL, best, off));
+                const uint32_t bal = __ballot_sync(FULL, mine == best);
+                const uint32_t gbits = GL == 32 ? bal : (bal >> (lane & ~(uint32_t)(GL - 1))) & ((1u << (GL & 31)) - 1u);
+                bj = (uint32_t)(__ffs(gbits) - 1) + GL * (best & ((1u << ush) - 1u));
             } else {
                 const A ae = it.e & use, al = it.l & use;
                 A bv = amax<A>();
@@ -557,8 +584,8 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
             // update needs no warp barrier (the shuffles already order the lanes)
             if ((bj & (GL - 1)) == gl) {
                 Pair2<A> el = EL[bj];
-                el.a += it.e;
-                el.b += it.l;
+                el.a += it.e << ush;
+                el.b += it.l << ush;
                 EL[bj] = el;  // FL: formed by the first build_lists (or fl_sums for m == 1)
                 set_apos(apos, pos, bj, wide);
             }
@@ -912,7 +939,9 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
                              u64& cmax, PhaseTimer& ph) {
     const uint32_t m = p.m;
     for (uint32_t j = gl; j < m; j += GL) {
-        EL[j] = PK ? Pair2<A>{(A)j, (A)(j + co)} : Pair2<A>{0, 0};  // co: the LPT probe offset
+        // co: the LPT probe offset; the plain variant's lane-local LPT keys carry k = j / GL
+        EL[j] = PK ? Pair2<A>{(A)j, (A)(j + co)}
+                   : (sh >= 0x100u ? Pair2<A>{(A)(j / GL), (A)(j / GL + co)} : Pair2<A>{0, 0});
         FL[j] = Pair2<A>{0, 0};
     }
     __syncwarp(FULL);
@@ -938,6 +967,10 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         if (PK) {  // drop the probe offset: plain packed keys from here on
             for (uint32_t j = gl; j < m; j += GL) EL[j].b -= (A)co;
             __syncwarp(FULL);
+        } else if (sh >= 0x100u) {  // lane-local LPT keys -> plain sums
+            for (uint32_t j = gl; j < m; j += GL)
+                EL[j] = Pair2<A>{(A)(EL[j].a >> (sh & 0xFFu)), (A)((EL[j].b - co) >> (sh & 0xFFu))};
+            __syncwarp(FULL);
         }
         ph.mark(0);
         if (m >= 2 && p.R > 0)
@@ -962,8 +995,22 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
 template <typename A, bool PK, int GL, bool SM, bool O4>
 __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     if (p.hdr->variant != p.want_variant) return;  // another variant runs
-    const uint32_t sh = PK ? p.hdr->shift : 0u;
-    const uint32_t co = PK ? p.hdr->offs : 0u;  // LPT probe offset (lpt_pass)
+    uint32_t sh = PK ? p.hdr->shift : 0u;
+    uint32_t co = PK ? p.hdr->offs : 0u;  // LPT probe offset (lpt_pass)
+    if constexpr (!PK && sizeof(A) == 4) {
+        // plain 32-bit variant (the packed bound fails, e.g. m large): the LPT still runs on
+        // packed keys when the bucket index local to a lane (k = j / GL, kb bits) fits --
+        // the same bound as the packed variant with kb instead of s = bits(m - 1);
+        // sh = 0x100 | kb marks it for lpt_pass, co = C << kb the probe offset
+        const uint32_t q = (p.m + GL - 1) / GL;
+        uint32_t kb = 0;
+        while ((1u << kb) < q) ++kb;
+        const u64 bound = (p.hdr->sum_e + p.hdr->sum_l + p.m - 1) / p.m + 2 * p.hdr->max_key + p.hdr->max_ld;
+        if (!p.exhaustive && p.m > 0 && kb < 32 && bound < (1ull << (32 - kb))) {
+            sh = 0x100u | kb;
+            co = (uint32_t)(p.hdr->max_ld << kb);
+        }
+    }
     extern __shared__ __align__(128) uint8_t smem[];
     Tbl<A, SM> T;
     if (SM) {

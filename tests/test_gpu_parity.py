@@ -206,6 +206,25 @@ def test_balance_packed_offset_bound(D, O, side):
     check_balance(D, O, q, plan, K=512, R=8, G=8, seed=(9, side + 1), c0=0, c1=512)
 
 
+@pytest.mark.parametrize("n_mb, l_dp", [(350, 2), (100, 1), (37, 3)])
+def test_balance_lane_local_packed_lpt(D, O, n_mb, l_dp):
+    # bucket sums too large for the packed variant's s = bits(m - 1) index bits but small
+    # enough for the lane-local index (k = j / GL): the plain variant's LPT runs on packed
+    # (v << kb | k) keys with cross-lane ties resolved by a ballot -- many identical items make
+    # exact ties of (v, k) across lanes frequent
+    m = n_mb * l_dp
+    plan = dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=3, l_dp=l_dp, n_mb=n_mb)
+    rng = np.random.default_rng(m)
+    n = 2000
+    q = rng.integers(100000, 900000, (4, n)).astype(np.uint32)
+    same = rng.random(n) < 0.6
+    q[:, same] = np.array([300000, 600000, 250000, 500000], np.uint32)[:, None]
+    s = max(1, int(np.ceil(np.log2(m))))
+    assert _packed_margin(q, m) >= (1 << (32 - s))   # not the packed variant
+    check_balance(D, O, q, plan, K=256, R=6, G=8, seed=(m, 5), c0=0, c1=64)
+    check_balance(D, O, q, plan, K=256, R=0, G=1, seed=(m, 6), c0=0, c1=16)
+
+
 def test_balance_64bit_path(D, O, presets):
     # 1 ns ticks: config 2's bucket sums exceed 2^32 -> 64-bit candidate kernel
     p = presets[2]
