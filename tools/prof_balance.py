@@ -3,6 +3,7 @@
     python tools/prof_balance.py --config 5 --K 8192 [--reps 2]
 """
 import argparse
+import json
 import os
 import sys
 import time
@@ -21,16 +22,18 @@ ap.add_argument("--K", type=int, default=8192)
 ap.add_argument("--R", type=int, default=-1)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--mode", type=int, default=0, help="16 = DFLOP_MODE_ORDER4")
+ap.add_argument("--plan", default="", help='JSON plan (e.g. a config-4 Stage-B plan), else the preset\'s')
 a = ap.parse_args()
 p = synth.presets()[a.config]
+plan = json.loads(a.plan) if a.plan else p.plan
 R = p.R if a.R < 0 else a.R
 t, f, x = (torch.from_numpy(v.astype(np.uint32).view(np.int32)).cuda() for v in p.features(0))
-_, ticks = D.predict_costs(p.model, p.plan, t, f, x, want_f32=False)
+_, ticks = D.predict_costs(p.model, plan, t, f, x, want_f32=False)
 for rep in range(a.reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    r = D.balance_microbatches(ticks, p.plan, a.K, R, p.G, p.seed(0), mode=a.mode)
+    r = D.balance_microbatches(ticks, plan, a.K, R, p.G, p.seed(0), mode=a.mode)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
