@@ -92,13 +92,25 @@ __global__ void __launch_bounds__(256) k_predict(PredictGrids grids, PredictLaun
     uint32_t* tk = cost_ticks ? cost_ticks + (size_t)blockIdx.y * plan_stride : nullptr;
     uint32_t ovf = 0;
     const uint32_t nq = VEC ? n / 4 : n;
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    const uint32_t q_first = blockIdx.x * blockDim.x + threadIdx.x, q_step = gridDim.x * blockDim.x;
+    // VEC: the next iteration's three 16-byte feature loads are issued before this iteration's
+    // arithmetic, so two iterations' loads are in flight per thread (HBM latency hiding)
+    uint4 na = make_uint4(0, 0, 0, 0), nb = na, nc = na;
+    if (VEC && q_first < nq) {
+        na = __ldg(reinterpret_cast<const uint4*>(tiles) + q_first);
+        nb = __ldg(reinterpret_cast<const uint4*>(frames) + q_first);
+        nc = __ldg(reinterpret_cast<const uint4*>(text) + q_first);
+    }
+    for (uint32_t q = q_first; q < nq; q += q_step) {
         uint32_t tv[4], fv[4], xv[4];
         const int cnt = VEC ? 4 : 1;
         if (VEC) {
-            const uint4 a = __ldg(reinterpret_cast<const uint4*>(tiles) + q);
-            const uint4 b = __ldg(reinterpret_cast<const uint4*>(frames) + q);
-            const uint4 c = __ldg(reinterpret_cast<const uint4*>(text) + q);
+            const uint4 a = na, b = nb, c = nc;
+            if (q + q_step < nq) {
+                na = __ldg(reinterpret_cast<const uint4*>(tiles) + q + q_step);
+                nb = __ldg(reinterpret_cast<const uint4*>(frames) + q + q_step);
+                nc = __ldg(reinterpret_cast<const uint4*>(text) + q + q_step);
+            }
             tv[0] = a.x; tv[1] = a.y; tv[2] = a.z; tv[3] = a.w;
             fv[0] = b.x; fv[1] = b.y; fv[2] = b.z; fv[3] = b.w;
             xv[0] = c.x; xv[1] = c.y; xv[2] = c.z; xv[3] = c.w;
