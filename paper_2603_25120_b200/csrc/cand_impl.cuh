@@ -287,6 +287,30 @@ DFLOP_DEV void each_entry(const uint4 v, uint32_t blk, bool wide, uint32_t m, F&
     }
 }
 
+// each_entry for a one-byte assignment with the 16 entries of the block visited from entry
+// `rot` on (f(pos, j) for pos = blk*16 + (e + rot) % 16): lanes holding consecutive blocks
+// then read item records 16*rot bytes apart -- distinct shared-memory banks -- instead of
+// all reading the same bank (the blocks are 256 bytes of records apart)
+template <typename F>
+DFLOP_DEV void each_entry_rot(const uint4 v, uint32_t blk, uint32_t rot, uint32_t m, F&& f) {
+    // rotate the 16 bytes right by rot (< 16) bytes: byte e of r = byte (e + rot) % 16 of v
+    const uint32_t q = rot >> 2, sh = 8u * (rot & 3u);
+    // words rotated by q (two select stages, no dynamic register indexing), then bytes by sh
+    const bool q1 = q & 1u, q2 = q & 2u;
+    const uint32_t a0 = q1 ? v.y : v.x, a1 = q1 ? v.z : v.y, a2 = q1 ? v.w : v.z, a3 = q1 ? v.x : v.w;
+    const uint32_t r[4] = {q2 ? a2 : a0, q2 ? a3 : a1, q2 ? a0 : a2, q2 ? a1 : a3};
+    uint32_t u[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u[i] = __funnelshift_r(r[i], r[(i + 1) & 3], sh);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint32_t j = (u[k] >> (8 * b)) & 0xFFu;
+            if (j < m) f(blk * 16 + ((4 * k + b + rot) & 15u), j);
+        }
+}
+
 // CSR member lists of all m buckets from the assignment: cnt[j] members of bucket j at
 // csr[off[j] ..], off[j+1] - off[j] = (LPT count) + sigma.  Two 16-byte L2 passes (count,
 // then scatter); the list order is irrelevant (the pair search is a keyed minimum).
@@ -301,13 +325,18 @@ DFLOP_DEV void build_lists(const CandParams& p, const Tbl<A, SM>& T, const uint8
     for (uint32_t j = gl; j < m; j += GL) cnt[j] = 0;
     __syncwarp(FULL);
     if (FL) {
-        for (uint32_t b = gl; b < nblk; b += GL)
-            each_entry(__ldcg(ap + b), b, wide, m, [&](uint32_t pos, uint32_t j) {
-                atomicAdd(&cnt[j], 1u);
-                const ItemRec<A> r = T.item(pos);
-                atomicAdd(&FL[j].a, r.ef);
-                atomicAdd(&FL[j].b, r.lf);
-            });
+        auto acc = [&](uint32_t pos, uint32_t j) {
+            atomicAdd(&cnt[j], 1u);
+            const ItemRec<A> r = T.item(pos);
+            atomicAdd(&FL[j].a, r.ef);
+            atomicAdd(&FL[j].b, r.lf);
+        };
+        for (uint32_t b = gl; b < nblk; b += GL) {
+            if (wide)
+                each_entry(__ldcg(ap + b), b, true, m, acc);
+            else  // the record loads of the group's lanes on distinct banks
+                each_entry_rot(__ldcg(ap + b), b, gl & 15u, m, acc);
+        }
     } else {
         for (uint32_t b = gl; b < nblk; b += GL)
             each_entry(__ldcg(ap + b), b, wide, m, [&](uint32_t, uint32_t j) { atomicAdd(&cnt[j], 1u); });
