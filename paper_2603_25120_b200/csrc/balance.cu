@@ -360,7 +360,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     };
     // shared-memory copies of the first `cap` members of j* and j': about twice the mean list
     // length, shrunk (not below 32) while that buys resident candidates -- occupancy hides the
-    // latency of the shared-memory and shuffle chains (config 5: cap 128 -> 96 raises 72 -> 80
+    // latency of the shared-memory and shuffle chains (config 5: cap 128 -> 104 raises 72 -> 80
     // candidates per SM, -6.7%; 768-thread blocks would need <= 80 registers: +37%)
     uint32_t cap = std::min(128u, std::max(32u, next_pow2(2 * std::max(1u, per_bucket))));
     {
