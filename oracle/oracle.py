@@ -69,11 +69,32 @@ class OrcBParams(C.Structure):
 _lib = None
 
 
+def build_variant(src_text: str, tag: str) -> str:
+    """Compile a MODIFIED copy of the oracle source (mutation tests of the pins,
+    tests/test_oracle_worked.py) into /tmp; returns the .so path.  Never used by lib()."""
+    import tempfile
+    d = tempfile.mkdtemp(prefix=f"orc_{tag}_")
+    src = os.path.join(d, "dflop_oracle.c")
+    with open(src, "w") as f:
+        f.write(src_text)
+    so = os.path.join(d, "liboracle.so")
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared", "-I" + HERE,
+                           "-o", so, src, "-lm"])
+    return so
+
+
 def lib():
     global _lib
     if _lib is None:
         build()
-        L = C.CDLL(LIB_PATH)
+        _lib = load(LIB_PATH)
+    return _lib
+
+
+def load(path: str):
+    """ctypes handle of an oracle build with every signature declared."""
+    if True:
+        L = C.CDLL(path)
         P = C.POINTER
         u32p, u64p, f64p = P(C.c_uint32), P(C.c_uint64), P(C.c_double)
         L.orc_philox4x32_10.argtypes = [u32p, u32p, u32p]
@@ -111,8 +132,7 @@ def lib():
         L.orc_stage_a_all.restype = C.c_uint64
         L.orc_stage_a_top.argtypes = [u64p, C.c_uint64, C.c_uint32, u64p]
         L.orc_stage_a_top.restype = C.c_uint32
-        _lib = L
-    return _lib
+    return L
 
 
 def _p(a: np.ndarray, t):

@@ -47,15 +47,17 @@ def plan_of(p):
 
 
 # ------------------------------------------------------------------ a1 predict
+@pytest.mark.parametrize("e_attn", [0, 1])
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
-def test_predict_parity(D, O, presets, k):
+def test_predict_parity(D, O, presets, k, e_attn):
     p = presets[k]
     pl = plan_of(p)
+    model = dict(p.model, e_attn=e_attn)     # e_attn = 1: in-tile encoder attention 4*h_E*E_seq^2 (R1)
     for b in (0, 1):
         (t, f, x), (dt, df, dx) = feats(p, b)
-        cf64, cq, st, _ = O.predict(p.model, pl, t, f, x)
+        cf64, cq, st, _ = O.predict(model, pl, t, f, x)
         assert st == 0
-        f32, ticks = D.predict_costs(p.model, pl, dt, df, dx)
+        f32, ticks = D.predict_costs(model, pl, dt, df, dx)
         g = f32.cpu().numpy().astype(np.float64)
         ref = cf64 / p.model["tick_ns"]
         assert np.all((ref == 0) == (g == 0))
@@ -63,6 +65,24 @@ def test_predict_parity(D, O, presets, k):
         assert rel.max() <= 1e-5, rel.max()
         q = host_u32(ticks).astype(np.int64)
         assert np.all(np.abs(q - cq.astype(np.int64)) <= 1 + 1e-5 * cq)
+
+
+@pytest.mark.parametrize("e_attn", [0, 1])
+def test_predict_worked_example(D, O, e_attn):
+    """The hand-derived worked example (tests/golden/predict_worked.txt: non-unit shapes,
+    knots that are not powers of two, E_tp != L_tp) through the C-ABI: fp32 within 1e-5 of
+    the exact values, ticks equal to the fixture's."""
+    from test_oracle_worked import load_predict_fixture
+    model, plan, items, costs = load_predict_fixture()
+    model = dict(model, e_attn=e_attn)
+    t, f, x = (np.array([it[j] for it in items], np.uint32) for j in (1, 2, 3))
+    f32, ticks = D.predict_costs(model, plan, dev_u32(t), dev_u32(f), dev_u32(x))
+    g, q = f32.cpu().numpy().astype(np.float64), host_u32(ticks)
+    for i, c in enumerate(c for c in costs if c["e_attn"] == e_attn):
+        for k in range(4):
+            exact = float(c["ns"][k])
+            assert (g[k, i] == 0) == (exact == 0) and abs(g[k, i] - exact) <= 1e-5 * exact, (c["name"], k)
+        assert [int(v) for v in q[:, i]] == c["ticks"], c["name"]
 
 
 @pytest.mark.parametrize("n", [0, 1, 3, 5, 4097])
@@ -314,18 +334,20 @@ def test_search_fixed_equals_balance(D, O, presets):
     assert (host_u32(res["assign"]) == o["assign"]).all()
 
 
-def test_search_alg1_stage_a_and_b(D, O, presets):
+@pytest.mark.parametrize("e_attn", [0, 1])
+def test_search_alg1_stage_a_and_b(D, O, presets, e_attn):
     p = presets[4]
+    model = dict(p.model, e_attn=e_attn)
     (t, f, x), (dt, df, dx) = feats(p)
     cl = p.cluster
     n_cfg = len(O.enumerate_configs(cl["n_gpus"], cl["gpus_per_node"]))
     sa = torch.empty(6_541_832, dtype=torch.int64, device="cuda")
     K, P = 8, 4
-    res = D.search_plans(p.model, dt, df, dx, K=K, R=p.R, G=p.G, seed=p.seed(0), cluster=cl, mem=p.mem(),
+    res = D.search_plans(model, dt, df, dx, K=K, R=p.R, G=p.G, seed=p.seed(0), cluster=cl, mem=p.mem(),
                          gbs=p.gbs, top_p=P, stage_a_out=sa)
     assert res["n_configs"] == n_cfg == 7194 and res["n_pairs"] == 6_541_832
-    mb, ms = O.batch_means(p.model, t, f, x)
-    T_orc, cfgs = O.stage_a_all(p.model, p.mem(), cl["n_gpus"], cl["gpus_per_node"], p.gbs, mb, ms)
+    mb, ms = O.batch_means(model, t, f, x)
+    T_orc, cfgs = O.stage_a_all(model, p.mem(), cl["n_gpus"], cl["gpus_per_node"], p.gbs, mb, ms)
     T_gpu = host_u64(sa)
     # fp64 with identical, FMA-free operation order on both sides: expected bit-identical
     assert (T_gpu == T_orc).all(), np.count_nonzero(T_gpu != T_orc)
@@ -342,7 +364,7 @@ def test_search_alg1_stage_a_and_b(D, O, presets):
         c = cfgs[e]
         pl = dict(e_tp=int(c[0]), e_pp=int(c[1]), e_dp=int(c[2]), l_tp=int(c[3]), l_pp=int(c[4]), l_dp=int(c[5]),
                   n_mb=i)
-        _, ticks = D.predict_costs(p.model, pl, dt, df, dx, want_f32=False)
+        _, ticks = D.predict_costs(model, pl, dt, df, dx, want_f32=False)
         o = O.balance_threaded(host_u32(ticks), pl, K, p.R, p.G, p.seed(0), per_candidate=False)
         key = (o["T"], rank, o["c"])
         if best is None or key < best[0]:
