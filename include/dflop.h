@@ -438,6 +438,31 @@ dflop_status dflop_get_unique_id(uint8_t id[128]);
 dflop_status dflop_comm_init(const uint8_t id[128], int rank, int world, int device, dflop_comm** comm);
 dflop_status dflop_comm_destroy(dflop_comm* comm);
 
+/* ---------------------------------------------------------------- sharding protocol
+ * The host arithmetic dflop_search_plans / dflop_search_plans_batches run around their NCCL
+ * collectives (P:796 the communicator; P:738 the argmin over candidates; P:491-497
+ * Eq. (1) over batches).  Pure host functions: no CUDA call, usable without a GPU (the gloo
+ * test drives the same protocol on CPU).  No pointer is retained.
+ *
+ * dflop_shard_range  candidates [*begin, *end) = [floor(K*rank/world), floor(K*(rank+1)/world))
+ *                    of rank `rank`; Philox counters use the global id, so the winner does not
+ *                    depend on world.  INVALID_ARGUMENT: world == 0, rank >= world, NULL outputs.
+ * dflop_owner_of     the rank whose range holds candidate c (UINT32_MAX if c >= K).
+ * dflop_pack_key     min(T, 2^40 - 1) << 24 | (id & 0xFFFFFF): the integer minimum over keys is
+ *                    the lexicographic minimum of (T, id) (R18); one 8-byte MIN all-reduce.  A
+ *                    saturated T is reported by the kernels' DFLOP_DEV_MAKESPAN_OVERFLOW bit.
+ * dflop_select_plan  keys: host u64 [P][D], reduced over ranks (UINT64_MAX = no candidate);
+ *                    batch_n: host u32 [D] batch sizes or NULL (an empty batch contributes 0).
+ *                    *win_p = argmin over p of (sum_b (keys[p][b] >> 24), p); objective: host
+ *                    u64 [P] or NULL, the sums (UINT64_MAX for a plan with a missing key).
+ *                    UNSUPPORTED ("no candidate evaluated", *win_p = UINT32_MAX) when no plan
+ *                    has all its keys; INVALID_ARGUMENT for NULL keys/win_p or P, D == 0. */
+dflop_status dflop_shard_range(uint32_t K, uint32_t rank, uint32_t world, uint32_t* begin, uint32_t* end);
+uint32_t dflop_owner_of(uint32_t K, uint32_t c, uint32_t world);
+uint64_t dflop_pack_key(uint64_t T, uint32_t id);
+dflop_status dflop_select_plan(const uint64_t* keys, uint32_t P, uint32_t D, const uint32_t* batch_n,
+                               uint32_t* win_p, uint64_t* objective);
+
 #ifdef __cplusplus
 }
 #endif

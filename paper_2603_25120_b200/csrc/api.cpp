@@ -439,20 +439,6 @@ static dflop_status get_config_table(uint32_t n_gpus, uint32_t node, uint32_t gb
     return DFLOP_OK;
 }
 
-static void shard(uint32_t K, int g, int G, uint32_t* b, uint32_t* e) {
-    *b = (uint32_t)(((uint64_t)K * g) / G);
-    *e = (uint32_t)(((uint64_t)K * (g + 1)) / G);
-}
-
-static int owner_of(uint32_t K, uint32_t c, int G) {
-    for (int g = 0; g < G; ++g) {
-        uint32_t b, e;
-        shard(K, g, G, &b, &e);
-        if (c >= b && c < e) return g;
-    }
-    return 0;
-}
-
 // workspace regions of the search
 struct SearchLayout {
     size_t o_costs, o_results, o_assigns, o_bcast, o_key, o_stage_a, o_top, o_feas, o_status, o_bal, total;
@@ -598,7 +584,7 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
     // balance workspace: exact for a fixed plan, bounded for Algorithm 1 (plans unknown yet)
     const int G = comm ? comm->world : 1, g = comm ? comm->rank : 0;
     uint32_t cb, cend;
-    shard(sp->K, g, G, &cb, &cend);
+    dflop_shard_range(sp->K, (uint32_t)g, (uint32_t)G, &cb, &cend);
     size_t bal_bytes = 0;
     if (alg1) {
         bal_bytes = balance_bound(n_max, std::max(1u, m_max), std::max(1u, cend - cb), dev);
@@ -760,34 +746,26 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
         if (!j || cudaEventRecord(j, ss[k]) != cudaSuccess) return cuda_status(cudaGetLastError(), "join event");
         if ((ce = cudaStreamWaitEvent(s, j, 0)) != cudaSuccess) return cuda_status(ce, "join wait");
     }
-    // ---- per (plan, batch) local keys, one NCCL min all-reduce of the [P*D] key array
-    std::vector<dflop_cand_result> hres(n_pairs_b);
-    ce = cudaMemcpyAsync(hres.data(), results, n_pairs_b * sizeof(dflop_cand_result), cudaMemcpyDeviceToHost, s);
-    uint32_t hstatus = 0;
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&hstatus, d_status, 4, cudaMemcpyDeviceToHost, s);
-    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
-    if (ce != cudaSuccess) return cuda_status(ce, "stage B readback");
-    std::vector<uint64_t> keys(n_pairs_b + 1);
-    for (uint32_t q = 0; q < n_pairs_b; ++q) {
-        keys[q] = hres[q].key;
-        if (hres[q].key != ~0ull) hstatus |= hres[q].status;
-    }
-    uint32_t gstatus = hstatus;
+    // ---- per (plan, batch) local keys gathered on the device, one NCCL min all-reduce of the
+    // [P*D] key array (+ a MAX of the two status flags) in place, one readback for the host's
+    // plan choice (protocol.cpp: dflop_select_plan)
+    if ((ce = gather_keys_launch(results, n_pairs_b, d_status, d_key, s)) != cudaSuccess)
+        return cuda_status(ce, "gather keys");
     if (comm && G > 1) {
-        // the status bits travel as a max over per-bit flags so that any rank's bit survives
-        uint32_t bits[2] = {hstatus & 1u, (hstatus >> 1) & 1u};
-        memcpy(&keys[n_pairs_b], bits, 8);
-        ce = cudaMemcpyAsync(d_key, keys.data(), (n_pairs_b + 1) * 8, cudaMemcpyHostToDevice, s);
-        if (ce != cudaSuccess) return cuda_status(ce, "key upload");
         uint32_t* d_bits = reinterpret_cast<uint32_t*>(d_key + n_pairs_b);
         ncclResult_t r = ncclGroupStart();
         if (r == ncclSuccess) r = ncclAllReduce(d_key, d_key, n_pairs_b, ncclUint64, ncclMin, comm->comm, s);
         if (r == ncclSuccess) r = ncclAllReduce(d_bits, d_bits, 2, ncclUint32, ncclMax, comm->comm, s);
         if (r == ncclSuccess) r = ncclGroupEnd();
         if ((st = nccl_status(r, "ncclAllReduce(min keys)")) != DFLOP_OK) return st;
-        ce = cudaMemcpyAsync(keys.data(), d_key, (n_pairs_b + 1) * 8, cudaMemcpyDeviceToHost, s);
-        if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
-        if (ce != cudaSuccess) return cuda_status(ce, "key readback");
+    }
+    std::vector<uint64_t> keys(n_pairs_b + 1);
+    ce = cudaMemcpyAsync(keys.data(), d_key, (n_pairs_b + 1) * 8, cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) return cuda_status(ce, "key readback");
+    uint32_t gstatus = 0;
+    {
+        uint32_t bits[2];
         memcpy(bits, &keys[n_pairs_b], 8);
         gstatus = bits[0] | (bits[1] << 1);
     }
@@ -795,28 +773,16 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
     // (T_B, p, c) -- the same choice
     uint32_t win_p = 0xFFFFFFFFu;
     uint64_t best_obj = ~0ull;
-    for (uint32_t p = 0; p < np; ++p) {
-        uint64_t obj = 0;
-        bool ok = true;
-        for (uint32_t b = 0; b < D; ++b) {
-            const uint64_t k = keys[p * D + b];
-            if (off[b + 1] == off[b]) continue;  // an empty batch contributes 0
-            if (k == ~0ull) {
-                ok = false;
-                break;
-            }
-            obj += k >> 24;
+    {
+        std::vector<uint32_t> batch_n(D);
+        std::vector<uint64_t> obj(np);
+        for (uint32_t b = 0; b < D; ++b) batch_n[b] = off[b + 1] - off[b];
+        if ((st = dflop_select_plan(keys.data(), np, D, batch_n.data(), &win_p, obj.data())) != DFLOP_OK) return st;
+        best_obj = obj[win_p];
+        for (uint32_t p = 0; p < np; ++p) {
+            if (plan_objective) plan_objective[p] = obj[p];
+            if (plans_out) plans_out[p] = plans[p];
         }
-        if (plan_objective) plan_objective[p] = ok ? obj : ~0ull;
-        if (plans_out) plans_out[p] = plans[p];
-        if (ok && obj < best_obj) {
-            best_obj = obj;
-            win_p = p;
-        }
-    }
-    if (win_p == 0xFFFFFFFFu) {
-        set_error("no candidate evaluated");
-        return DFLOP_ERR_UNSUPPORTED;
     }
     // ---- every batch's winner of plan win_p: the owner packs, NCCL broadcasts (G > 1)
     dflop_cand_result first{};
@@ -832,7 +798,7 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
             const uint64_t key = keys[q];
             const uint32_t id = (uint32_t)(key & 0xFFFFFFull);
             win_c = id - win_p * sp->K;
-            owner = owner_of(sp->K, win_c, G);
+            owner = (int)dflop_owner_of(sp->K, win_c, (uint32_t)G);
             if (g == owner) {
                 ce = cudaMemcpyAsync(bcast, &results[q], sizeof(dflop_cand_result), cudaMemcpyDeviceToDevice, s);
                 if (ce == cudaSuccess && nb > 0)

@@ -275,6 +275,37 @@ cudaError_t groups_launch(const uint32_t* assign, uint32_t n, uint32_t m, uint32
     return cudaGetLastError();
 }
 
+// a5 exchange input, device-resident: key[q] = results[q].key for the
+// [P x D] (plan, batch) results, and in key[n] two u32 flags -- bit 0 and bit 1 of the status
+// (the predict status OR the status of every result that evaluated a candidate) -- so the
+// flags survive a MAX all-reduce as an OR.  One block.
+__global__ void k_gather_keys(const dflop_cand_result* __restrict__ res, uint32_t n,
+                              const uint32_t* __restrict__ d_status, uint64_t* key) {
+    __shared__ uint32_t s_or;
+    if (threadIdx.x == 0) s_or = *d_status;
+    __syncthreads();
+    uint32_t acc = 0;
+    for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) {
+        const dflop_cand_result r = res[q];
+        key[q] = r.key;
+        if (r.key != ~0ull) acc |= r.status;
+    }
+    acc = __reduce_or_sync(0xFFFFFFFFu, acc);
+    if ((threadIdx.x & 31u) == 0 && acc) atomicOr(&s_or, acc);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t* bits = reinterpret_cast<uint32_t*>(key + n);
+        bits[0] = s_or & 1u;
+        bits[1] = (s_or >> 1) & 1u;
+    }
+}
+
+cudaError_t gather_keys_launch(const dflop_cand_result* res, uint32_t n, const uint32_t* d_status, uint64_t* key,
+                               cudaStream_t s) {
+    k_gather_keys<<<1, 256, 0, s>>>(res, n, d_status, key);
+    count_launches(1);
+    return cudaGetLastError();
+}
 
 // diagnostic phase counters of the candidate kernel (timing builds only)
 static unsigned long long* phase_counters() {

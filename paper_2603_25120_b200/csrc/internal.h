@@ -130,6 +130,8 @@ size_t exact_ws_bytes(uint32_t n, uint32_t m, const dflop_plan* p);
 dflop_status exact_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p, uint64_t node_budget,
                           const uint32_t* init_assign, void* ws, dflop_exact_result* out, uint32_t* assign,
                           cudaStream_t s);
+cudaError_t gather_keys_launch(const dflop_cand_result* res, uint32_t n, const uint32_t* d_status, uint64_t* key,
+                               cudaStream_t s);
 cudaError_t groups_launch(const uint32_t* assign, uint32_t n, uint32_t m, uint32_t* offsets, uint32_t* items,
                           void* ws, cudaStream_t s);
 

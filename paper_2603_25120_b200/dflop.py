@@ -27,7 +27,7 @@ EXPORTS = ["dflop_abi_version", "dflop_last_error", "dflop_release_caches", "dfl
            "dflop_balance_microbatches", "dflop_simulate_1f1b", "dflop_index_groups", "dflop_search_plans",
            "dflop_get_unique_id", "dflop_comm_init", "dflop_comm_destroy", "dflop_profile_enable",
            "dflop_profile_read", "dflop_search_plans_batches", "dflop_exact_cmax", "dflop_order_search",
-           "dflop_route_plan"]
+           "dflop_route_plan", "dflop_shard_range", "dflop_owner_of", "dflop_pack_key", "dflop_select_plan"]
 
 
 class DflopError(RuntimeError):
@@ -144,9 +144,15 @@ def lib():
         L.dflop_comm_destroy.argtypes = [vp]
         L.dflop_profile_enable.argtypes = [C.c_int]
         L.dflop_profile_read.argtypes = [P(Profile), C.c_int]
+        L.dflop_shard_range.argtypes = [u32, u32, u32, P(u32), P(u32)]
+        L.dflop_owner_of.argtypes = [u32, u32, u32]
+        L.dflop_pack_key.argtypes = [u64, u32]
+        L.dflop_select_plan.argtypes = [P(u64), u32, u32, P(u32), P(u32), P(u64)]
         for f in EXPORTS:
-            if f not in ("dflop_abi_version", "dflop_last_error"):
+            if f not in ("dflop_abi_version", "dflop_last_error", "dflop_owner_of", "dflop_pack_key"):
                 getattr(L, f).restype = C.c_int32
+        L.dflop_owner_of.restype = u32
+        L.dflop_pack_key.restype = u64
         _lib = L
     return _lib
 
@@ -235,6 +241,37 @@ def _u32(t):
 
 
 # ---------------------------------------------------------------- API (same names as the C ABI)
+# ---------------------------------------------------------------- sharding protocol (host)
+def shard_range(K: int, rank: int, world: int):
+    """Candidates [begin, end) of `rank` (dflop_shard_range; no GPU needed)."""
+    b, e = C.c_uint32(), C.c_uint32()
+    _check(lib().dflop_shard_range(K, rank, world, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def owner_of(K: int, c: int, world: int) -> int:
+    return lib().dflop_owner_of(K, c, world)
+
+
+def pack_key(T: int, cand_id: int) -> int:
+    return lib().dflop_pack_key(T, cand_id)
+
+
+def select_plan(keys, P: int, D: int, batch_n: Optional[Sequence[int]] = None):
+    """keys: P*D reduced u64 keys (plan-major).  Returns (win_p, objective[P])."""
+    k = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64))
+    assert k.size == P * D
+    obj = np.zeros(P, np.uint64)
+    win = C.c_uint32()
+    bn = None
+    if batch_n is not None:
+        bn = np.ascontiguousarray(np.asarray(batch_n, dtype=np.uint32))
+    u64p, u32p = C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)
+    _check(lib().dflop_select_plan(k.ctypes.data_as(u64p), P, D, bn.ctypes.data_as(u32p) if bn is not None else None,
+                                   C.byref(win), obj.ctypes.data_as(u64p)))
+    return win.value, obj
+
+
 def abi_version() -> int:
     return int(lib().dflop_abi_version())
 

@@ -19,7 +19,7 @@ import torch
 import torch.distributed as dist
 
 from paper_2603_25120_b200 import dflop as D
-from paper_2603_25120_b200 import sharding, synth
+from paper_2603_25120_b200 import synth
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
@@ -49,7 +49,7 @@ if rank == 0:
     ref = run(None)
     ok = (res["makespan"], res["cand"], res["cmax"]) == (ref["makespan"], ref["cand"], ref["cmax"])
     ok = ok and bool((assign == ref["assign"].cpu().numpy()).all())
-    ok = ok and res["owner_rank"] == sharding.owner_of(a.K, res["cand"], world)
+    ok = ok and res["owner_rank"] == D.owner_of(a.K, res["cand"], world)
     ok = ok and res["plan"] == ref["plan"] and res["stage_a_rank"] == ref["stage_a_rank"]
     if a.batches:
         ok = ok and [b["makespan"] for b in res["batches"]] == [b["makespan"] for b in ref["batches"]]
