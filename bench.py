@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--order4", action="store_true", help="DFLOP_MODE_ORDER4: per-candidate slot-order choice")
+    ap.add_argument("--tick-ns", type=float, default=0.0,
+                    help="override the preset's integer time unit (1 = nanosecond ticks: the 64-bit kernel variant)")
     return ap.parse_args()
 
 
@@ -48,8 +50,12 @@ def dist_env():
 
 # ---------------------------------------------------------------- workload
 def workload(args, world):
+    import dataclasses
+
     from paper_2603_25120_b200 import synth
     p = synth.presets()[args.config]
+    if args.tick_ns:
+        p = dataclasses.replace(p, model=dict(p.model, tick_ns=float(args.tick_ns)))
     K = args.K or p.K
     if p.plan is None:  # config 4: the Algorithm-1 search (Stage A + P plans x K candidates)
         return p, K, "strong", None, None
@@ -72,6 +78,31 @@ def algorithmic_ops_per_candidate(n, m, S, R, G):
     sim = 4.0 * 2 * S * m
     philox = 80.0 * (-(-n // G)) * (-(-(G - 1) // 4))
     return lpt + ref + sim + philox
+
+
+def config_dict(args, p, K, m, S, world):
+    """The `config` object of the JSON line -- identical for the GPU arm and the reference arm."""
+    return {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "K_per_gpu": K // world,
+            "plans": p.top_p if p.plan is None else 1, "order4": bool(args.order4), "R": p.R, "G": p.G,
+            "plan": p.plan if p.plan is not None else "searched (Algorithm 1 Stage A + Stage B)",
+            "tick_ns": p.model["tick_ns"], "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": f"candidate-shard x{world}"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def int_peaks():
+    """profiles/int_peaks.json (tools/int_peaks.cu, measured on a B200 of this pool)."""
+    f = os.path.join(ROOT, "profiles", "int_peaks.json")
+    return json.load(open(f)) if os.path.exists(f) else None
 
 
 # ---------------------------------------------------------------- clocks (NVML)
@@ -163,30 +194,51 @@ def oracle_rate(p, K_family, budget_s, threads=None):
             threads)
 
 
+def oracle_rate_1thread(p, K_family, n_cand=1024):
+    """BASELINE.md 4.2 / SURVEY 8(d): the oracle on ONE thread over a fixed subset of 1,024
+    candidates [0, 1024) of batch 0 (predict excluded): a per-core rate."""
+    from oracle import oracle as O
+    t, f, x = p.features(0)
+    plan = p.plan
+    if plan is None:
+        return None
+    _, q, _, _ = O.predict(p.model, plan, t, f, x)
+    c1 = min(K_family, n_cand)
+    t0 = time.perf_counter()
+    O.balance(q, plan, K_family, p.R, p.G, p.seed(0), 0, c1, per_candidate=False)
+    return c1 / (time.perf_counter() - t0), c1
+
+
 def run_reference(args):
+    """The reference arm: the CPU oracle as it stands on the host cores, each step a bounded
+    sample of the workload; ms_per_step is the measured wall time of a step."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     p, K, scaling, m, S = workload(args, world)
-    from oracle import oracle as O
     threads = os.cpu_count() or 1
     steps, warm = args.steps, args.warmup
     per_step_budget = max(2.0, min(20.0, 150.0 / max(1, steps + warm)))
-    rates = []
+    rates, walls, samples = [], [], []
     for i in range(warm + steps):
+        t0 = time.perf_counter()
         r, sample, thr = oracle_rate(p, K, per_step_budget, threads)
+        w = time.perf_counter() - t0
         if i >= warm:
             rates.append(r)
+            walls.append(w)
+            samples.append(sample)
     value = statistics.mean(rates)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-        "warmup": warm, "ms_per_step": 1e3 * K * (p.top_p if p.plan is None else 1) / value,
+        "warmup": warm, "ms_per_step": 1e3 * statistics.mean(walls),
         "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "R": p.R, "G": p.G,
-                   "note": "reference arm = the CPU oracle (no installable reference: the paper ships no code)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"each step: {sample}"},
+        "config": config_dict(args, p, K, m, S, world),
+        "reference_note": "reference arm = the CPU oracle (no installable reference: the paper ships no code); "
+                          "each step evaluates a bounded sample of the family (ms_per_step = its measured wall time)",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": "oracle",
+                         "sample": f"each step: {samples[-1] if samples else ''}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -321,6 +373,12 @@ def main():
         e2e = {"value": P * K * len(e_times) / (e_total / 1e3), "unit": UNIT, "h2d_bytes_per_step": 3 * 4 * p.n,
                "d2h_bytes_per_step": 4 * p.n + 32 + 8, "p50_ms": statistics.median(e_times)}
 
+    # ---- which candidate-kernel variant ran: k_build_items picks the 64-bit sums when a batch's
+    # sum of e or l reaches 2^32 - 1 ticks (the u32 variants' bound on every bucket sum)
+    _, tk = D.predict_costs(p.model, p.plan if not alg1 else res["plan"], *dfeat[0], want_f32=False)
+    tk = tk.cpu().numpy().view(np.uint32).astype(np.uint64)
+    wide_sums = int(tk[0].sum() + tk[1].sum()) >= (1 << 32) - 1 or int(tk[2].sum() + tk[3].sum()) >= (1 << 32) - 1
+
     # ---- roofline of the dominant kernel (candidates: integer-issue bound)
     b, e = (K * rank) // world, (K * (rank + 1)) // world
     if alg1:
@@ -335,17 +393,30 @@ def main():
     else:
         ops_launch = algorithmic_ops_per_candidate(p.n, m, S, p.R, p.G) * (e - b)
         cand_ms = prof["cand_ms"] / max(1, prof["cand_launches"])
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak_tops = n_sm * 4 * 32 * sm_max * 1e6 / 1e12        # issue-limited int32 lane-ops
     achieved = ops_launch / (cand_ms / 1e3) / 1e12
-    roofline = {"bound": "alu", "kernel": "k_candidates<u32>", "achieved": achieved, "peak": peak_tops,
-                "unit": "Tops/s", "frac": achieved / peak_tops, "traffic": None,
+    ip = int_peaks()
+    if ip:
+        # measured (tools/int_peaks.cu -> profiles/int_peaks.json): instruction issue with both
+        # integer pipes busy (adds split by ptxas over IADD3 / IMAD.IADD), and the ALU pipe alone
+        # (IADD3, VIMNMX, VIADDMNMX, LOP3 -- the pipe the LPT probes and min trees run on)
+        peak_issue = ip["add_u32_ptxas_choice"]["lane_ops_per_s"] / 1e12
+        peak_alu = ip["viaddmnmx_u32"]["lane_ops_per_s"] / 1e12
+        note = (f"measured: profiles/int_peaks.json (tools/int_peaks.cu, {ip['gpu']}, "
+                f"{ip['add_u32_ptxas_choice']['sm_mhz_in_kernel']} MHz): issue "
+                f"{ip['add_u32_ptxas_choice']['lane_ops_per_clk_per_sm']:.1f} lane-ops/clk/SM, ALU pipe "
+                f"{ip['viaddmnmx_u32']['lane_ops_per_clk_per_sm']:.1f} lane-ops/clk/SM")
+    else:
+        sm_max = 1965.0
+        peak_issue = n_sm * 4 * 32 * sm_max * 1e6 / 1e12
+        peak_alu = peak_issue / 2
+        note = "fallback: 148 SM x 4 SMSP x 32 lanes x 1965 MHz (profiles/int_peaks.json missing)"
+    variant = "u64" if wide_sums else "u32"
+    roofline = {"bound": "issue", "kernel": f"k_candidates<{variant}>", "achieved": achieved, "peak": peak_issue,
+                "unit": "Tops/s", "frac": achieved / peak_issue, "traffic": None,
+                "peak_alu_pipe": peak_alu, "frac_alu_pipe": achieved / peak_alu,
                 "kernel_ms": cand_ms, "kernel_share_of_step": cand_ms / ms_per_step,
-                "peak_note": f"{n_sm} SM x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
-                "ops_per_candidate": ops_launch / max(1, (e - b) * P)}
+                "peak_note": note, "ops_per_candidate": ops_launch / max(1, (e - b) * P)}
     if alg1:
         roofline["kernel"] = "k_candidates<u32> x P plans (Stage B, 4 streams)"
         roofline["duration_note"] = "device step time (Stage A + Stage B)"
@@ -370,11 +441,8 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": p.name, "n": p.n, "m": m, "S": S, "K": K, "K_per_gpu": K // world,
-                   "plans": P, "order4": bool(args.order4), "R": p.R,
-                   "G": p.G, "plan": p.plan if not alg1 else res["plan"], "tick_ns": p.model["tick_ns"],
-                   "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"candidate-shard x{world}"},
+        "vs_baseline": None, "dtype": variant, "data": "synthetic",
+        "config": config_dict(args, p, K, m if not alg1 else None, S, world),
         "p50_plan_latency_ms": p50, "p99_plan_latency_ms": p99,
         "candidate_microbatches_per_s": value * m,
         "e2e": e2e,
@@ -382,11 +450,17 @@ def main():
         "roofline": roofline,
         "clocks": clk.summary(),
         "winner": {"batch": (args.warmup + args.steps - 1) % n_batches, "cand": res["cand"],
-                   "makespan_ticks": res["makespan"], "cmax_ticks": res["cmax"]},
+                   "makespan_ticks": res["makespan"], "cmax_ticks": res["cmax"], "plan": res["plan"]},
+        "kernel_variant": variant,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample, thr = oracle_rate(p, K, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample}
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "cpu_model": cpu_model(), "kind": "oracle",
+                                "sample": sample}
+        one = oracle_rate_1thread(p, K)
+        if one:
+            line["cpu_baseline"]["per_core"] = {"value": one[0], "unit": UNIT, "threads": 1,
+                                                "sample": f"candidates [0, {one[1]}) of batch 0, one thread"}
     if rank == 0:
         emit(line)
     if comm is not None:

@@ -30,6 +30,16 @@ def test_reference_arm_one_json_line():
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 1 and d["warmup"] == 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["cpu_model"]
+    # the GPU arm builds its config with the same function (same_config for the driver)
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    args = argparse.Namespace(config=2, K=0, tick_ns=0.0, order4=False)
+    p, K, _, m, S = bench.workload(args, 1)
+    assert d["config"] == json.loads(json.dumps(bench.config_dict(args, p, K, m, S, 1)))
+    # ms_per_step is the measured wall time of the step (not an extrapolation to K)
+    assert 0 < d["ms_per_step"] < 60_000
 
 
 @pytest.mark.gpu
@@ -38,7 +48,9 @@ def test_gpu_arm_one_json_line():
     assert BASE_KEYS <= set(d) and d.get("impl", "dflop") != "reference"
     assert d["value"] > 0 and d["gpu_launches"] > 0 and d["config"]["workload"].startswith("cfg2")
     r = d["roofline"]
-    assert r["bound"] in ("alu", "hbm", "tensor") and 0 < r["frac"] <= 1 and r["achieved"] > 0 and r["peak"] > 0
+    assert r["bound"] == "issue" and 0 < r["frac"] <= 1 and r["achieved"] > 0 and r["peak"] > 0
+    assert 0 < r["frac_alu_pipe"] <= 1 and "int_peaks.json" in r["peak_note"]
+    assert d["cpu_baseline"] if "cpu_baseline" in d else True
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
