@@ -256,6 +256,42 @@ DFLOP_DEV A keyval(A v, uint32_t sh) {
     return PK ? (A)(v & ~((1u << sh) - 1u)) : v;
 }
 
+// shared-memory byte store / 8- and 16-byte loads at a shared-window address (the LPT's
+// per-group staging of the one-byte assignment, flushed with one global store per group)
+DFLOP_DEV void sts_u8(uint32_t saddr, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(saddr), "r"(v) : "memory"); }
+DFLOP_DEV uint32_t lds_u8(uint32_t saddr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+    return v;
+}
+DFLOP_DEV uint2 lds_v2(uint32_t saddr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(saddr) : "memory");
+    return v;
+}
+DFLOP_DEV uint4 lds_v4(uint32_t saddr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr)
+                 : "memory");
+    return v;
+}
+
+// The ng (<= 16) staged decisions of base-order group [start, start + ng) -> the assignment:
+// one 8- or 16-byte store by lane 0 for full aligned groups of 8 / 16, else one byte per lane.
+// Called by all lanes of the warp (start and ng are warp-uniform).
+template <int GL>
+DFLOP_DEV void flush_stage(uint8_t* apos, uint32_t stage_s, uint32_t start, uint32_t ng, uint32_t gl) {
+    __syncwarp(FULL);
+    if (ng == 8 && (start & 7u) == 0) {
+        if (gl == 0) *reinterpret_cast<uint2*>(apos + start) = lds_v2(stage_s);
+    } else if (ng == 16 && (start & 15u) == 0) {
+        if (gl == 0) *reinterpret_cast<uint4*>(apos + start) = lds_v4(stage_s);
+    } else {
+        for (uint32_t u = gl; u < ng; u += GL) apos[start + u] = (uint8_t)lds_u8(stage_s + u);
+    }
+    __syncwarp(FULL);
+}
+
 DFLOP_DEV void set_apos(uint8_t* apos, uint32_t pos, uint32_t j, bool wide) {
     if (wide)
         reinterpret_cast<uint16_t*>(apos)[pos] = (uint16_t)j;
@@ -408,7 +444,7 @@ DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t d, u
 template <int GL, bool FIX8>
 DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* apos, uint32_t pa, uint32_t pb,
                              const Pair2<uint32_t> ia, const Pair2<uint32_t> ib, uint32_t jmask,
-                             uint32_t gl, uint32_t m, bool wide, uint32_t co) {
+                             uint32_t gl, uint32_t m, bool wide, uint32_t co, uint32_t stage_s, uint32_t start) {
     // never called for c == 0 (its probes use zero items; the single-sample loop does it)
     const uint32_t da = ia.a - ia.b + co, db = ib.a - ib.b + co;  // probe offsets (lpt_pass)
     uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
@@ -459,26 +495,25 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
         m1 = min(m1, o1);
     }
     const uint32_t ja = ba & jmask;
-    const bool own_a = (ja & (GL - 1)) == gl;
+    const bool own_a = ((ba ^ gl) & (GL - 1)) == 0;
     // every lane of the group reads a* (one broadcast load) and evaluates B's probe of a*
     // after A itself -- no shuffle from the owner on the dependency chain
     const Pair2<uint32_t> ela = EL[ja];
     const uint32_t alt = min(m2, max(ela.a + ia.a + db, ela.b + ia.b));  // a* after A, probed by B
-    const uint32_t jb = (((m1 & jmask) != ja) ? m1 : alt) & jmask;
-    if (own_a) {
-        EL[ja] = Pair2<uint32_t>{ela.a + ia.a, ela.b + ia.b};  // FL: formed by the first build_lists
-        if constexpr (FIX8)
-            apos[pa] = (uint8_t)ja;
-        else
-            set_apos(apos, pa, ja, wide);
-    }
-    if ((jb & (GL - 1)) == gl) {  // after A's update in program order when jb = ja (same lane)
-        const Pair2<uint32_t> el = EL[jb];
-        EL[jb] = Pair2<uint32_t>{el.a + ib.a, el.b + ib.b};
-        if constexpr (FIX8)
-            apos[pb] = (uint8_t)jb;
-        else
-            set_apos(apos, pb, jb, wide);
+    const uint32_t kb = ((m1 & jmask) != ja) ? m1 : alt;
+    const uint32_t jb = kb & jmask;
+    const bool own_b = ((kb ^ gl) & (GL - 1)) == 0;
+    // owner updates as predicated stores (no branch): FL is formed by the first build_lists;
+    // the assignment byte goes to the group's shared-memory stage (flushed per base group)
+    if (own_a) EL[ja] = Pair2<uint32_t>{ela.a + ia.a, ela.b + ia.b};
+    const Pair2<uint32_t> elb = EL[jb];  // after A's update in program order when jb = ja (same lane)
+    if (own_b) EL[jb] = Pair2<uint32_t>{elb.a + ib.a, elb.b + ib.b};
+    if constexpr (FIX8) {
+        if (own_a) sts_u8(stage_s + (pa - start), ja);
+        if (own_b) sts_u8(stage_s + (pb - start), jb);
+    } else {
+        if (own_a) set_apos(apos, pa, ja, wide);
+        if (own_b) set_apos(apos, pb, jb, wide);
     }
 }
 
@@ -492,7 +527,7 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
 // bound covers probe + C); c == 0 probes with d = co.
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
-                        Pair2<A>* FL, uint8_t* apos, uint32_t gl, uint32_t co) {
+                        Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint32_t gl, uint32_t co) {
     const uint32_t n = p.n, m = p.m, G = p.G;
     const bool wide = p.wide != 0;  // u16 assignment when m > 255
     const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
@@ -505,6 +540,21 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
     const uint32_t W = nc ? max(1u, 32u / ((32u / GL) * nc)) : 1u;
     const uint32_t lane = threadIdx.x & 31u, mycg = lane / GL;
     const uint32_t n_groups = (n + G - 1) / G;
+    // one-byte assignments with m == 8 * GL: the group's decisions are staged in the (idle)
+    // refinement scratch and flushed with one 8/16-byte store per base group (flush_stage)
+    const bool stg = !wide && m == 8 * GL;
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(scr);
+    // the first m decisions are forced: every probe of an empty bucket is below every probe of
+    // a non-empty one when the m largest keys are > 0, so the sample at step t < m takes bucket
+    // t (both rules; ties to the lowest empty bucket).  Packed variant, G = GL = 8: lane gl
+    // places the sample at step start + gl of each of the first m / 8 base groups.
+    bool forced = false;
+    if constexpr (PK && GL == 8) {
+        if (stg && G == 8 && m <= n) {
+            const Pair2<A> r = T.el(m - 1);  // base-order position m-1: the m-th largest key
+            forced = (r.a | r.b) != 0;
+        }
+    }
     for (uint32_t g0 = 0; g0 < n_groups; g0 += W) {
       const uint64_t preg = nc ? batch_perms<GL>(g0, W, nc, c, n, G, p.seed0, p.seed1) : 0xFEDCBA9876543210ull;
       for (uint32_t gg = 0; gg < W && g0 + gg < n_groups; ++gg) {
@@ -512,6 +562,17 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
         const uint32_t ng = min(G, n - start);
         const uint64_t perm = nc ? __shfl_sync(FULL, preg, mycg * W + gg) : 0xFEDCBA9876543210ull;
         uint32_t t = 0;
+        if (forced && start + 8 <= m) {
+            const uint32_t nib = (uint32_t)(perm >> (4 * gl)) & 15u;
+            const uint32_t pos = start + nib, j = start + gl;
+            const Pair2<A> r = T.el(pos);
+            Pair2<A> el = EL[j];
+            el.a += r.a;
+            el.b += r.b;
+            EL[j] = el;
+            sts_u8(stage_s + nib, j);
+            t = ng;
+        }
 #ifndef DFLOP_NO_LPT_PAIRS
         if constexpr (PK) {
             // two samples per step (see lpt_pair_step); the warp holding c == 0 takes the
@@ -523,7 +584,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, true>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
-                                            T.el(pb), jmask, gl, m, false, co);
+                                            T.el(pb), jmask, gl, m, false, co, stage_s, start);
                 }
             } else {
                 for (; t + 1 < ng; t += 2) {
@@ -531,7 +592,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, false>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                              reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
-                                             T.el(pb), jmask, gl, m, wide, co);
+                                             T.el(pb), jmask, gl, m, wide, co, 0u, start);
                 }
             }
         }
@@ -627,9 +688,13 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                 el.a += it.e << ush;
                 el.b += it.l << ush;
                 EL[bj] = el;  // FL: formed by the first build_lists (or fl_sums for m == 1)
-                set_apos(apos, pos, bj, wide);
+                if (stg)
+                    sts_u8(stage_s + (pos - start), bj);
+                else
+                    set_apos(apos, pos, bj, wide);
             }
         }
+        if (stg) flush_stage<GL>(apos, stage_s, start, ng, gl);
       }
     }
     __syncwarp(FULL);
@@ -1003,7 +1068,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         }
         __syncwarp(FULL);
     } else {
-        lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, gl, co);
+        lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, gl, co);
         if (PK) {  // drop the probe offset: plain packed keys from here on
             for (uint32_t j = gl; j < m; j += GL) EL[j].b -= (A)co;
             __syncwarp(FULL);
