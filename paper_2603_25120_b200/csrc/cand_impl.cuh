@@ -181,7 +181,11 @@ DFLOP_DEV uint64_t batch_perms(uint32_t g0, uint32_t W, uint32_t nc, uint32_t c,
     const uint32_t cc = __shfl_sync(FULL, c, cg * GL);
     const uint32_t start = (g0 + gg) * G;
     const uint32_t ng = start < n ? min(G, n - start) : 0u;
+    // the Fisher-Yates on a 32-bit word when every position of the group is < 8 (G <= 8:
+    // half the shift/xor work of the 64-bit form; the high nibbles stay the identity)
     uint64_t perm = 0xFEDCBA9876543210ull;
+    uint32_t p32 = 0x76543210u;
+    const bool narrow = G <= 8;  // warp-uniform
     for (uint32_t pc = 0; pc < nc; ++pc) {
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
@@ -197,12 +201,18 @@ DFLOP_DEV uint64_t batch_perms(uint32_t g0, uint32_t W, uint32_t nc, uint32_t c,
             if (idx + 1 < ng) {
                 const uint32_t tt = ng - 1 - idx;
                 const uint32_t r = mulhi32(word, tt + 1);
-                const uint64_t a = (perm >> (4 * tt)) & 15ull, b = (perm >> (4 * r)) & 15ull;
-                const uint64_t x = a ^ b;
-                perm ^= (x << (4 * tt)) | (x << (4 * r));
+                if (narrow) {
+                    const uint32_t x = ((p32 >> (4 * tt)) ^ (p32 >> (4 * r))) & 15u;
+                    p32 ^= (x << (4 * tt)) | (x << (4 * r));
+                } else {
+                    const uint64_t a = (perm >> (4 * tt)) & 15ull, b = (perm >> (4 * r)) & 15ull;
+                    const uint64_t x = a ^ b;
+                    perm ^= (x << (4 * tt)) | (x << (4 * r));
+                }
             }
         }
     }
+    if (narrow) perm = 0xFEDCBA9800000000ull | p32;
     if (cc < 2 || lane >= cw * W) perm = 0xFEDCBA9876543210ull;
     return perm;
 }
@@ -226,6 +236,8 @@ struct Tbl {
     const ItemRec<A>* it;
     const uint16_t* pi16;   // SM
     const uint32_t* pi32;   // !SM
+    uint32_t it_s;          // SM: shared-window address of it (explicit ld.shared: no per-use
+                            // generic-to-shared conversion in the LPT loop)
     DFLOP_DEV ItemRec<A> item(uint32_t pos) const {
         if (SM) return it[pos];
         if (sizeof(A) == 4) {
@@ -237,7 +249,16 @@ struct Tbl {
         return ItemRec<A>{(A)a.x, (A)a.y, (A)b.x, (A)b.y};
     }
     DFLOP_DEV Pair2<A> el(uint32_t pos) const {
-        if (SM) return *reinterpret_cast<const Pair2<A>*>(it + pos);
+        if (SM) {
+            if constexpr (sizeof(A) == 4) {
+                Pair2<A> r;
+                // the table is read-only after staging: no volatile, no clobber (free to schedule)
+                asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.a), "=r"(r.b) : "r"(it_s + pos * 16u));
+                return r;
+            } else {
+                return *reinterpret_cast<const Pair2<A>*>(it + pos);
+            }
+        }
         const ItemRec<A> r = item(pos);
         return Pair2<A>{r.e, r.l};
     }
@@ -258,7 +279,7 @@ DFLOP_DEV A keyval(A v, uint32_t sh) {
 
 // shared-memory byte store / 8- and 16-byte loads at a shared-window address (the LPT's
 // per-group staging of the one-byte assignment, flushed with one global store per group)
-DFLOP_DEV void sts_u8(uint32_t saddr, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(saddr), "r"(v) : "memory"); }
+DFLOP_DEV void sts_u8(uint32_t saddr, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(saddr), "r"(v)); }
 DFLOP_DEV uint32_t lds_u8(uint32_t saddr) {
     uint32_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
@@ -537,7 +558,9 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
     const uint32_t ush = (!PK && sizeof(A) == 4 && sh >= 0x100u) ? (sh & 0xFFu) : 0u;
     const bool lanepk = !PK && sizeof(A) == 4 && sh >= 0x100u;
     const uint32_t nc = (G - 1 + 3) / 4;  // Philox calls per group
-    const uint32_t W = nc ? max(1u, 32u / ((32u / GL) * nc)) : 1u;
+    // base groups per permutation batch: every lane of the warp runs one Fisher-Yates (W = 32 /
+    // candidate groups per warp) as long as the Philox words fit the 4 calls per lane of batch_perms
+    const uint32_t W = nc ? max(1u, min((uint32_t)GL, 128u / ((32u / GL) * nc))) : 1u;
     const uint32_t lane = threadIdx.x & 31u, mycg = lane / GL;
     const uint32_t n_groups = (n + G - 1) / G;
     // one-byte assignments with m == 8 * GL: the group's decisions are staged in the (idle)
@@ -1126,10 +1149,12 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         for (uint32_t i = threadIdx.x; i < p.n; i += blockDim.x) pi16[i] = (uint16_t)__ldg(p.pos_item + i);
         __syncthreads();
         T.it = reinterpret_cast<const ItemRec<A>*>(smem);
+        T.it_s = (uint32_t)__cvta_generic_to_shared(smem);
         T.pi16 = pi16;
         T.pi32 = nullptr;
     } else {
         T.it = reinterpret_cast<const ItemRec<A>*>(p.items);
+        T.it_s = 0;
         T.pi16 = nullptr;
         T.pi32 = p.pos_item;
     }
