@@ -548,7 +548,7 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
 // bound covers probe + C); c == 0 probes with d = co.
 template <typename A, bool PK, int GL, bool SM>
 DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
-                        Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint32_t gl, uint32_t co) {
+                        Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint32_t gl, uint32_t co, bool forced) {
     const uint32_t n = p.n, m = p.m, G = p.G;
     const bool wide = p.wide != 0;  // u16 assignment when m > 255
     const A use = (c == 0) ? (A)0 : amax<A>();  // c == 0 probes the current load
@@ -567,17 +567,13 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
     // refinement scratch and flushed with one 8/16-byte store per base group (flush_stage)
     const bool stg = !wide && m == 8 * GL;
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(scr);
-    // the first m decisions are forced: every probe of an empty bucket is below every probe of
-    // a non-empty one when the m largest keys are > 0, so the sample at step t < m takes bucket
-    // t (both rules; ties to the lowest empty bucket).  Packed variant, G = GL = 8: lane gl
-    // places the sample at step start + gl of each of the first m / 8 base groups.
-    bool forced = false;
-    if constexpr (PK && GL == 8) {
-        if (stg && G == 8 && m <= n) {
-            const Pair2<A> r = T.el(m - 1);  // base-order position m-1: the m-th largest key
-            forced = (r.a | r.b) != 0;
-        }
-    }
+    // The first m decisions are forced when every one of the m largest items has e > 0 and
+    // l > 0 (`forced`, k_candidates): at step t < m buckets 0..t-1 hold one such item each and
+    // the rest are empty, so every non-empty probe -- max(E_k + e, L_k + l) with E_k, L_k > 0,
+    // or the current load max(E_k, L_k) > 0 of the c = 0 rule -- is strictly above the empty
+    // buckets' max(e, l) (resp. 0), and the lowest empty bucket, t, wins.  (With an item of
+    // e = 0 or l = 0 among them an earlier bucket can tie the empty ones and take the sample,
+    // so the shortcut is off.)  Lane gl places the forced steps of its own buckets.
     for (uint32_t g0 = 0; g0 < n_groups; g0 += W) {
       const uint64_t preg = nc ? batch_perms<GL>(g0, W, nc, c, n, G, p.seed0, p.seed1) : 0xFEDCBA9876543210ull;
       for (uint32_t gg = 0; gg < W && g0 + gg < n_groups; ++gg) {
@@ -585,16 +581,22 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
         const uint32_t ng = min(G, n - start);
         const uint64_t perm = nc ? __shfl_sync(FULL, preg, mycg * W + gg) : 0xFEDCBA9876543210ull;
         uint32_t t = 0;
-        if (forced && start + 8 <= m) {
-            const uint32_t nib = (uint32_t)(perm >> (4 * gl)) & 15u;
-            const uint32_t pos = start + nib, j = start + gl;
-            const Pair2<A> r = T.el(pos);
-            Pair2<A> el = EL[j];
-            el.a += r.a;
-            el.b += r.b;
-            EL[j] = el;
-            sts_u8(stage_s + nib, j);
-            t = ng;
+        if (forced && start < m) {  // warp-uniform
+            const uint32_t nf = min(ng, m - start);
+            for (uint32_t u = (gl + GL - start % GL) % GL; u < nf; u += GL) {
+                const uint32_t nib = (uint32_t)(perm >> (4 * u)) & 15u;
+                const uint32_t pos = start + nib, j = start + u;  // j % GL == gl: this lane's bucket
+                const Pair2<A> r = T.el(pos);
+                Pair2<A> el = EL[j];
+                el.a += r.a << ush;
+                el.b += r.b << ush;
+                EL[j] = el;
+                if (stg)
+                    sts_u8(stage_s + nib, j);
+                else
+                    set_apos(apos, pos, j, wide);
+            }
+            t = nf;
         }
 #ifndef DFLOP_NO_LPT_PAIRS
         if constexpr (PK) {
@@ -1064,7 +1066,7 @@ DFLOP_DEV u64 score_order4(const CandParams& p, uint32_t sh, const Pair2<A>* EL,
 template <typename A, bool PK, int GL, bool SM, bool O4>
 DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, uint32_t co, Pair2<A>* EL,
                              Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, u64& Tc,
-                             u64& cmax, PhaseTimer& ph) {
+                             u64& cmax, PhaseTimer& ph, bool forced) {
     const uint32_t m = p.m;
     for (uint32_t j = gl; j < m; j += GL) {
         // co: the LPT probe offset; the plain variant's lane-local LPT keys carry k = j / GL
@@ -1091,7 +1093,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         }
         __syncwarp(FULL);
     } else {
-        lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, gl, co);
+        lpt_pass<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, gl, co, forced);
         if (PK) {  // drop the probe offset: plain packed keys from here on
             for (uint32_t j = gl; j < m; j += GL) EL[j].b -= (A)co;
             __syncwarp(FULL);
@@ -1158,6 +1160,17 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         T.pi16 = nullptr;
         T.pi32 = p.pos_item;
     }
+    // forced first-m LPT decisions (lpt_pass): every item at base positions [0, m) has e > 0
+    // and l > 0 (warp-uniform; the exhaustive mode has no LPT)
+    bool forced = false;
+    if (!p.exhaustive && p.m >= 1 && p.m <= p.n) {
+        bool ok = true;
+        for (uint32_t q = threadIdx.x & 31u; q < p.m; q += 32) {
+            const Pair2<A> r = T.el(q);
+            ok = ok && r.a != 0 && r.b != 0;
+        }
+        forced = __all_sync(FULL, ok);
+    }
     const uint32_t grp = threadIdx.x / GL, gl = threadIdx.x % GL;
     const uint32_t cpb = blockDim.x / GL;
     uint8_t* base = smem + p.tbl_bytes + (size_t)grp * p.cand_bytes;
@@ -1189,7 +1202,7 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         const uint32_t c = valid ? cc : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
         u64 Tc, cmax;
-        run_candidate<A, PK, GL, SM, O4>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph);
+        run_candidate<A, PK, GL, SM, O4>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph, forced);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
         u64 key;
         if (Tc >= (1ull << 40)) {

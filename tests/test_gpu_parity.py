@@ -199,6 +199,47 @@ def test_balance_edge_cases(D, O, case):
         check_balance(D, O, q, plan, K=300, R=6, G=G, seed=(n, 3), c0=0, c1=40)
 
 
+def _forced_tie_costs(n_video, n_text, lt=2990):
+    """Videos (e = 3000, l = 5) and text-only samples (e = 0, l = lt <= 2995): a text sample's
+    bucket (E = 0, L = lt) probed by a later video gives max(0 + 3000, lt + 5) = 3000, the same
+    value as an empty bucket, so the video takes the (lower) text bucket."""
+    n = n_video + n_text
+    q = np.zeros((4, n), np.uint32)
+    for i in range(n):
+        if i % 2 == 0 and i // 2 < n_video or i // 2 >= n_text:
+            q[:, i] = (1000, 2000, 1, 4)          # e = 3000, l = 5
+        else:
+            q[:, i] = (0, 0, lt // 3, lt - lt // 3)  # e = 0, l = lt
+    return q
+
+
+@pytest.mark.parametrize("n_video,n_text,n_mb", [(36, 92, 64), (20, 30, 8), (100, 300, 256)])
+def test_balance_lpt_empty_bucket_ties(D, O, n_video, n_text, n_mb):
+    """The first-m LPT shortcut (lpt_pass) must stay off when one of the m largest samples has
+    e = 0 or l = 0: a perturbed order can put a text sample before a video of the same base
+    group, and the video then ties an empty bucket and takes the earlier, non-empty one."""
+    q = _forced_tie_costs(n_video, n_text)
+    plan = dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=1, l_dp=1, n_mb=n_mb)
+    check_balance(D, O, q, plan, K=512, R=4, G=8, seed=(5, 6), c0=0, c1=512)
+    if n_video < n_mb:  # the oracle's family has candidates whose first m steps are NOT "t -> bucket t"
+        order = O.base_order(q)
+        top = [int(order[t]) for t in range(n_mb)]
+        off = sum(sorted(int(O.run_candidate(q, plan, 512, 0, 8, (5, 6), c)[0][i]) for i in top) != list(range(n_mb))
+                  for c in range(2, 40))
+        assert off > 0
+
+
+def test_balance_lpt_forced_prefix(D, O):
+    """Every sample has e > 0 and l > 0 (config-4-like, m a third of n): the first m decisions
+    are forced; per-candidate results equal the oracle's step-by-step LPT."""
+    rng = np.random.default_rng(9)
+    n = 600
+    q = rng.integers(1, 4000, size=(4, n)).astype(np.uint32)
+    for n_mb, l_dp in ((200, 1), (96, 2), (64, 1), (8, 1)):
+        plan = dict(e_tp=1, e_pp=2, e_dp=1, l_tp=1, l_pp=2, l_dp=l_dp, n_mb=n_mb)
+        check_balance(D, O, q, plan, K=256, R=5, G=8, seed=(11, n_mb), c0=0, c1=256)
+
+
 def _packed_margin(q, m):
     """bound + C of the packed variant (k_build_items): ceil((sum e + sum l)/m) + 2 max key + max(l - e)+"""
     q = q.astype(np.int64)
