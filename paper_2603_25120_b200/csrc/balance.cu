@@ -494,6 +494,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     p.item_pos = item_pos;
     p.ops = prog.d_ops;
     p.levels = prog.d_levels;
+    p.dense = prog.d_dense;
     p.n_levels = prog.n_levels;
     p.hdr = hdr;
     p.slot_apos = slot_apos;

@@ -29,6 +29,7 @@ struct CandParams {
     const uint32_t* item_pos;    // [n] item index -> position (global)
     const uint32_t* ops;         // 1F1B slot program, n_ops entries
     const uint32_t* levels;      // n_levels + 1 offsets into ops
+    const uint32_t* dense;       // [n_levels][S] stage-indexed ops (0xFFFFFFFF: idle)
     BalanceHeader* hdr;
     uint8_t* slot_apos;          // [n_slots][2][apos_bytes]
     uint16_t* slot_csr;          // [n_slots][csr_len] refinement member lists (positions, CSR)

@@ -40,6 +40,7 @@ DFLOP_DEV A shfl_x(unsigned mask, A v, int off) {
 // identical control flow, so shuffles and warp barriers use the full mask; xor offsets below
 // GL keep each exchange inside its group.
 constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr uint32_t kNoOpDev = 0xFFFFFFFFu;  // idle stage in the level-dense 1F1B program
 
 // Diagnostic per-phase cycle counters (built only with -DDFLOP_TIMING, libdflop_timing.so):
 // 0 LPT, 1 refine j*/j', 2 refine member lists, 3 refine pairs, 4 refine reduce+apply,
@@ -1010,12 +1011,66 @@ DFLOP_DEV u64 score_replica(const CandParams& p, uint32_t sh, const Pair2<A>* EL
     return t;
 }
 
+// The same evaluation with each lane owning stages gl and gl + GL (S <= 2 GL): the level-dense
+// program gives every stage its op at each level (or none), the stage's running end time stays
+// in a register, and the next level's op codes are fetched one level ahead -- the dependent
+// chain of a level is one ring load, the max/add and the ring store.
+template <typename A, bool PK, int GL, typename Map>
+DFLOP_DEV u64 score_replica_ls(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr,
+                               uint32_t gl, uint32_t rho, Map&& slot_of) {
+    const uint32_t S = p.S, D = p.D, Dm = p.D - 1, NL = p.n_levels;
+    u64* FR = scr + S;  // same layout as score_replica (ORDER4's slot orders follow the rings)
+    u64* BR = FR + S * D;
+    const uint32_t s0 = gl, s1 = gl + GL;
+    const bool has1 = s1 < S;  // the second stage of this lane
+    u64 last0 = 0, last1 = 0;
+    uint32_t n0 = s0 < S ? __ldg(p.dense + s0) : kNoOpDev;
+    uint32_t n1 = has1 ? __ldg(p.dense + s1) : kNoOpDev;
+    auto run = [&](uint32_t op, uint32_t s, u64& last) {
+        const uint32_t kind = op_kind(op), k = op_mb(op);
+        const uint32_t j = slot_of(k) * p.l_dp + rho;
+        const Pair2<A> el = EL[j], fl = FL[j];
+        const bool enc = s < p.e_pp;
+        u64 dur, dep = 0;
+        if (kind == 0) {
+            dur = enc ? (u64)fl.a : (u64)fl.b;
+            if (s > 0) dep = FR[(s - 1) * D + (k & Dm)];
+        } else {
+            dur = enc ? (u64)(unpack<A, PK>(el.a, sh) - fl.a) : (u64)(unpack<A, PK>(el.b, sh) - fl.b);
+            dep = (s + 1 < S) ? BR[(s + 1) * D + (k & Dm)] : FR[s * D + (k & Dm)];
+        }
+        const u64 end = (last > dep ? last : dep) + dur;
+        last = end;
+        if (kind == 0)
+            FR[s * D + (k & Dm)] = end;
+        else
+            BR[s * D + (k & Dm)] = end;
+    };
+    for (uint32_t L = 0; L < NL; ++L) {
+        const uint32_t c0 = n0, c1 = n1;
+        if (L + 1 < NL) {  // next level's ops: independent of this level's results
+            const uint32_t* nx = p.dense + (size_t)(L + 1) * S;
+            n0 = s0 < S ? __ldg(nx + s0) : kNoOpDev;
+            n1 = has1 ? __ldg(nx + s1) : kNoOpDev;
+        }
+        if (c0 != kNoOpDev) run(c0, s0, last0);
+        if (c1 != kNoOpDev) run(c1, s1, last1);
+        __syncwarp(FULL);
+    }
+    u64 t = last0 > last1 ? last0 : last1;
+    t = max_reduce<u64, GL>(t, FULL);
+    __syncwarp(FULL);
+    return t;
+}
+
 template <typename A, bool PK, int GL>
 DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr,
                          uint32_t gl) {
     u64 T = 0;
+    const bool ls = p.dense != nullptr && p.S <= 2 * GL;  // uniform
     for (uint32_t rho = 0; rho < p.l_dp; ++rho) {
-        const u64 t = score_replica<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [](uint32_t k) { return k; });
+        const u64 t = ls ? score_replica_ls<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [](uint32_t k) { return k; })
+                         : score_replica<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [](uint32_t k) { return k; });
         T = t > T ? t : T;
     }
     return T;

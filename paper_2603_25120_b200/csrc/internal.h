@@ -53,8 +53,10 @@ struct SlotProgram {
     uint32_t S = 0, M = 0, D = 0;  // D = ring depth (power of two)
     const uint32_t* d_ops = nullptr;     // device copy, 2*S*M entries
     const uint32_t* d_levels = nullptr;  // device, n_levels + 1 offsets into d_ops
+    const uint32_t* d_dense = nullptr;   // device, [n_levels][S]: stage s's op at level L, or kNoOp
     uint32_t n_ops = 0, n_levels = 0;
 };
+constexpr uint32_t kNoOp = 0xFFFFFFFFu;
 // Builds (once per (S, M) and device) a topological order of the 1F1B DAG by Kahn levels.
 dflop_status get_slot_program(uint32_t S, uint32_t M, SlotProgram* out);
 void release_slot_programs();

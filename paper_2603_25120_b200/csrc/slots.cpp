@@ -31,7 +31,7 @@ inline uint32_t enc(uint32_t kind, uint32_t s, uint32_t k) { return (kind << 31)
 }  // namespace
 
 static void build_program(uint32_t S, uint32_t M, std::vector<uint32_t>& out, std::vector<uint32_t>& levels,
-                          uint32_t& D) {
+                          std::vector<uint32_t>& dense, uint32_t& D) {
     // per-stage op sequences; node id = s * 2M + t
     const uint32_t L_ = 2 * M, L = L_;
     std::vector<uint32_t> kind(S * L), mb(S * L);
@@ -119,6 +119,12 @@ static void build_program(uint32_t S, uint32_t M, std::vector<uint32_t>& out, st
     }
     D = 1;
     while (D < need) D <<= 1;
+    // the same order, level-dense: dense[L * S + s] = stage s's op at level L (kNoOp if idle),
+    // so a lane that owns stage s reads its op at a fixed stride (the candidate kernel's scorer)
+    const size_t nl = levels.size() - 1;
+    dense.assign(nl * S, kNoOp);
+    for (size_t L = 0; L < nl; ++L)
+        for (uint32_t q = levels[L]; q < levels[L + 1]; ++q) dense[L * S + ((out[q] >> 16) & 31u)] = out[q];
 }
 
 dflop_status get_slot_program(uint32_t S, uint32_t M, SlotProgram* out) {
@@ -131,9 +137,9 @@ dflop_status get_slot_program(uint32_t S, uint32_t M, SlotProgram* out) {
         *out = it->second.prog;
         return DFLOP_OK;
     }
-    std::vector<uint32_t> ops, levels;
+    std::vector<uint32_t> ops, levels, dense;
     uint32_t D = 1;
-    build_program(S, M, ops, levels, D);
+    build_program(S, M, ops, levels, dense, D);
     if (D > 16) {
         set_error("1F1B ring depth %u > 16 for S=%u M=%u", D, S, M);
         return DFLOP_ERR_UNSUPPORTED;
@@ -141,6 +147,7 @@ dflop_status get_slot_program(uint32_t S, uint32_t M, SlotProgram* out) {
     Entry e;
     std::vector<uint32_t> all(ops);
     all.insert(all.end(), levels.begin(), levels.end());
+    all.insert(all.end(), dense.begin(), dense.end());
     cudaError_t ce = cudaMalloc(&e.d_ops, all.size() * sizeof(uint32_t));
     if (ce != cudaSuccess) return cuda_status(ce, "slot program alloc");
     ce = cudaMemcpy(e.d_ops, all.data(), all.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
@@ -152,6 +159,7 @@ dflop_status get_slot_program(uint32_t S, uint32_t M, SlotProgram* out) {
     e.prog.n_ops = (uint32_t)ops.size();
     e.prog.n_levels = (uint32_t)levels.size() - 1;
     e.prog.d_levels = e.d_ops + ops.size();
+    e.prog.d_dense = e.prog.d_levels + levels.size();
     g_cache[key] = e;
     *out = e.prog;
     return DFLOP_OK;
