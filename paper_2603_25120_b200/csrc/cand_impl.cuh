@@ -1013,51 +1013,77 @@ DFLOP_DEV u64 score_replica(const CandParams& p, uint32_t sh, const Pair2<A>* EL
 
 // The same evaluation with each lane owning stages gl and gl + GL (S <= 2 GL): the level-dense
 // program gives every stage its op at each level (or none), the stage's running end time stays
-// in a register, and the next level's op codes are fetched one level ahead -- the dependent
-// chain of a level is one ring load, the max/add and the ring store.
-template <typename A, bool PK, int GL, typename Map>
+// in a register, the next level's op codes are fetched one level ahead, and the per-stage ring
+// addresses are fixed per lane -- a level is one branch-free op per stage: its bucket sums, its
+// dependency from the neighbour's ring, max/add, one ring store.
+template <typename A, bool PK>
+struct StageLane {
+    u64 last;          // end time of the stage's latest op
+    u64* fr_dep;       // F dependency ring (stage s-1; s = 0: own ring, masked)
+    u64* br_dep;       // B dependency ring (stage s+1; last stage: its own F ring)
+    u64* fr_own;
+    u64* br_own;
+    bool enc, has_fdep;
+};
+
+template <typename A, bool PK>
+DFLOP_DEV void stage_lane_init(StageLane<A, PK>& L, uint32_t s, uint32_t S, uint32_t D, uint32_t e_pp, u64* FR, u64* BR) {
+    L.last = 0;
+    L.enc = s < e_pp;
+    L.has_fdep = s > 0;
+    L.fr_own = FR + (size_t)s * D;
+    L.br_own = BR + (size_t)s * D;
+    L.fr_dep = s > 0 ? FR + (size_t)(s - 1) * D : L.fr_own;
+    L.br_dep = s + 1 < S ? BR + (size_t)(s + 1) * D : L.fr_own;
+}
+
+template <typename A, bool PK>
+DFLOP_DEV void stage_lane_op(StageLane<A, PK>& L, uint32_t op, const Pair2<A>* EL, const Pair2<A>* FL, uint32_t l_dp,
+                             uint32_t rho, uint32_t sh, uint32_t Dm) {
+    const bool act = op != kNoOpDev;
+    const uint32_t kind = op >> 31, k = act ? (op & 0xFFFFu) : 0u;
+    const uint32_t j = k * l_dp + rho;
+    const Pair2<A> el = EL[j], fl = FL[j];
+    const A fdur = L.enc ? fl.a : fl.b;
+    const A bdur = L.enc ? (A)(unpack<A, PK>(el.a, sh) - fl.a) : (A)(unpack<A, PK>(el.b, sh) - fl.b);
+    const u64 dur = kind ? (u64)bdur : (u64)fdur;
+    const uint32_t slot = k & Dm;
+    u64 dep = (kind ? L.br_dep : L.fr_dep)[slot];
+    dep = (kind || L.has_fdep) ? dep : 0ull;
+    const u64 end = (L.last > dep ? L.last : dep) + dur;
+    if (act) {
+        L.last = end;
+        (kind ? L.br_own : L.fr_own)[slot] = end;
+    }
+}
+
+template <typename A, bool PK, int GL>
 DFLOP_DEV u64 score_replica_ls(const CandParams& p, uint32_t sh, const Pair2<A>* EL, const Pair2<A>* FL, u64* scr,
-                               uint32_t gl, uint32_t rho, Map&& slot_of) {
-    const uint32_t S = p.S, D = p.D, Dm = p.D - 1, NL = p.n_levels;
+                               uint32_t gl, uint32_t rho) {
+    const uint32_t S = p.S, D = p.D, Dm = p.D - 1, NL = p.n_levels, l_dp = p.l_dp;
     u64* FR = scr + S;  // same layout as score_replica (ORDER4's slot orders follow the rings)
     u64* BR = FR + S * D;
     const uint32_t s0 = gl, s1 = gl + GL;
-    const bool has1 = s1 < S;  // the second stage of this lane
-    u64 last0 = 0, last1 = 0;
-    uint32_t n0 = s0 < S ? __ldg(p.dense + s0) : kNoOpDev;
-    uint32_t n1 = has1 ? __ldg(p.dense + s1) : kNoOpDev;
-    auto run = [&](uint32_t op, uint32_t s, u64& last) {
-        const uint32_t kind = op_kind(op), k = op_mb(op);
-        const uint32_t j = slot_of(k) * p.l_dp + rho;
-        const Pair2<A> el = EL[j], fl = FL[j];
-        const bool enc = s < p.e_pp;
-        u64 dur, dep = 0;
-        if (kind == 0) {
-            dur = enc ? (u64)fl.a : (u64)fl.b;
-            if (s > 0) dep = FR[(s - 1) * D + (k & Dm)];
-        } else {
-            dur = enc ? (u64)(unpack<A, PK>(el.a, sh) - fl.a) : (u64)(unpack<A, PK>(el.b, sh) - fl.b);
-            dep = (s + 1 < S) ? BR[(s + 1) * D + (k & Dm)] : FR[s * D + (k & Dm)];
-        }
-        const u64 end = (last > dep ? last : dep) + dur;
-        last = end;
-        if (kind == 0)
-            FR[s * D + (k & Dm)] = end;
-        else
-            BR[s * D + (k & Dm)] = end;
-    };
-    for (uint32_t L = 0; L < NL; ++L) {
+    const bool has0 = s0 < S, has1 = s1 < S;
+    StageLane<A, PK> L0, L1;
+    stage_lane_init(L0, has0 ? s0 : 0, S, D, p.e_pp, FR, BR);
+    stage_lane_init(L1, has1 ? s1 : 0, S, D, p.e_pp, FR, BR);
+    const uint32_t* dn = p.dense;
+    uint32_t n0 = has0 ? __ldg(dn + s0) : kNoOpDev;
+    uint32_t n1 = has1 ? __ldg(dn + s1) : kNoOpDev;
+    const bool any1 = __any_sync(FULL, has1);  // warp-uniform
+    for (uint32_t lv = 0; lv < NL; ++lv) {
         const uint32_t c0 = n0, c1 = n1;
-        if (L + 1 < NL) {  // next level's ops: independent of this level's results
-            const uint32_t* nx = p.dense + (size_t)(L + 1) * S;
-            n0 = s0 < S ? __ldg(nx + s0) : kNoOpDev;
-            n1 = has1 ? __ldg(nx + s1) : kNoOpDev;
+        if (lv + 1 < NL) {  // next level's ops: independent of this level's results
+            dn += S;
+            n0 = has0 ? __ldg(dn + s0) : kNoOpDev;
+            n1 = has1 ? __ldg(dn + s1) : kNoOpDev;
         }
-        if (c0 != kNoOpDev) run(c0, s0, last0);
-        if (c1 != kNoOpDev) run(c1, s1, last1);
+        stage_lane_op(L0, c0, EL, FL, l_dp, rho, sh, Dm);
+        if (any1) stage_lane_op(L1, c1, EL, FL, l_dp, rho, sh, Dm);
         __syncwarp(FULL);
     }
-    u64 t = last0 > last1 ? last0 : last1;
+    u64 t = L0.last > L1.last ? L0.last : L1.last;
     t = max_reduce<u64, GL>(t, FULL);
     __syncwarp(FULL);
     return t;
@@ -1069,7 +1095,7 @@ DFLOP_DEV u64 score_1f1b(const CandParams& p, uint32_t sh, const Pair2<A>* EL, c
     u64 T = 0;
     const bool ls = p.dense != nullptr && p.S <= 2 * GL;  // uniform
     for (uint32_t rho = 0; rho < p.l_dp; ++rho) {
-        const u64 t = ls ? score_replica_ls<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [](uint32_t k) { return k; })
+        const u64 t = ls ? score_replica_ls<A, PK, GL>(p, sh, EL, FL, scr, gl, rho)
                          : score_replica<A, PK, GL>(p, sh, EL, FL, scr, gl, rho, [](uint32_t k) { return k; });
         T = t > T ? t : T;
     }
