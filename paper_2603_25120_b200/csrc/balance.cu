@@ -91,6 +91,57 @@ __global__ void k_rank_sort(const u64* __restrict__ keys, uint32_t n, uint32_t* 
     }
 }
 
+// The same order by one CTA: a bitonic sort in shared memory of the composite keys
+// (2^34 - 1 - key) << 16 | i (keys < 2^33: sums of two u32 ticks; i < 2^16), ascending =
+// key descending, index ascending -- O(n log^2 n) instead of k_rank_sort's O(n^2) compares.
+// n <= kBitonicMax; N = next power of two, padded with all-ones keys (sort last).
+constexpr uint32_t kBitonicMax = 8192;
+__global__ void __launch_bounds__(1024) k_bitonic_order(const u64* __restrict__ keys, uint32_t n, uint32_t* order,
+                                                        uint32_t* item_pos) {
+    extern __shared__ u64 sk[];
+    uint32_t N = 1;
+    while (N < n) N <<= 1;
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x)
+        sk[i] = i < n ? ((((1ull << 34) - 1) - keys[i]) << 16) | i : ~0ull;
+    __syncthreads();
+    for (uint32_t k = 2; k <= N; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t t = threadIdx.x; t < N / 2; t += blockDim.x) {
+                const uint32_t lo = 2 * t - (t & (j - 1)), hi = lo + j;  // pair (lo, lo + j), lo's bit j clear
+                const bool up = (lo & k) == 0;
+                const u64 a = sk[lo], b = sk[hi];
+                if ((a > b) == up) {
+                    sk[lo] = b;
+                    sk[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+        const uint32_t i = (uint32_t)(sk[r] & 0xFFFFu);
+        order[r] = i;
+        item_pos[i] = r;
+    }
+}
+
+void order_launch_keys(const u64* keys, uint32_t n, uint32_t* order, uint32_t* item_pos, cudaStream_t s) {
+    if (n == 0) return;
+    if (n <= kBitonicMax) {
+        uint32_t N = 1;
+        while (N < n) N <<= 1;
+        static bool attr = false;  // 64 KB of shared memory at kBitonicMax
+        if (!attr) {
+            cudaFuncSetAttribute(k_bitonic_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBitonicMax * 8));
+            attr = true;
+        }
+        k_bitonic_order<<<1, std::min<uint32_t>(1024u, std::max(32u, N / 2)), (size_t)N * 8, s>>>(keys, n, order,
+                                                                                                    item_pos);
+    } else {
+        k_rank_sort<<<(n + 255) / 256, 256, 0, s>>>(keys, n, order, item_pos);
+    }
+}
+
 // Chooses the candidate-kernel variant and writes the per-position records.
 //   u32 when every bucket sum fits (sums of all e_i, l_i below 2^32 - 1);
 //   packed u32 when every LPT probe value plus the probe offset C = max_i max(l_i - e_i, 0)
@@ -484,7 +535,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
         const uint32_t gb = std::min<uint32_t>((n + 255) / 256, 592);
         const size_t rs = a.cost_stride ? a.cost_stride : n;
         k_prep_keys<<<gb, 256, 0, s>>>(a.cost_ticks, n, rs, hdr, keys);
-        k_rank_sort<<<(n + 255) / 256, 256, 0, s>>>(keys, n, order, item_pos);
+        order_launch_keys(keys, n, order, item_pos, s);
         k_build_items<<<gb, 256, 0, s>>>(a.cost_ticks, n, rs, a.sh.m, allow_pack, hdr, order, it32, it64);
     } else {
         k_build_items<<<1, 32, 0, s>>>(a.cost_ticks, 0, 0, a.sh.m, allow_pack, hdr, order, it32, it64);

@@ -379,7 +379,7 @@ dflop_status exact_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p,
     if (n > 0) {
         const uint32_t gb = std::min<uint32_t>((n + 255) / 256, 592);
         k_prep_keys<<<gb, 256, 0, s>>>(cost, n, n, bh, keys);
-        k_rank_sort<<<(n + 255) / 256, 256, 0, s>>>(keys, n, order, item_pos);
+        order_launch_keys(keys, n, order, item_pos, s);
         count_launches(2);
     }
     k_exact_init<<<1, 256, 0, s>>>(cost, n, m, order, init_assign, pe, pl, by_item, h);

@@ -114,6 +114,8 @@ size_t groups_ws_bytes(uint32_t n, uint32_t m);
 // a2 kernels shared by the balance and the exact solver (balance.cu; types from common.cuh)
 __global__ void k_prep_keys(const uint32_t* __restrict__ cost, uint32_t n, size_t rs, BalanceHeader* hdr, u64* keys);
 __global__ void k_rank_sort(const u64* __restrict__ keys, uint32_t n, uint32_t* order, uint32_t* item_pos);
+// LPT base order (rank sort above, or a one-CTA bitonic sort for n <= 8192)
+void order_launch_keys(const u64* keys, uint32_t n, uint32_t* order, uint32_t* item_pos, cudaStream_t s);
 #endif
 
 // ---------------------------------------------------------------- N4(b) routing plan (route.cu)
