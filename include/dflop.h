@@ -327,6 +327,9 @@ dflop_status dflop_index_groups(const uint32_t* assign, uint32_t n, uint32_t m, 
  *   assign         device u32[n] or NULL: the winner's bucket per sample.
  *   stage_a_out    device u64[stage_a_cap] or NULL: T_A of every pair in enumeration
  *                  order (UINT64_MAX = infeasible), written when stage_a_cap >= n_pairs.
+ * A Stage-B plan beyond the balancer's limits (E_pp + L_pp > 32 or N_mb * L_dp > 65535,
+ * possible from 34 GPUs on) is skipped: it is not balanced and never chosen (its objective
+ * is UINT64_MAX); UNSUPPORTED when every top-P plan is skipped.
  * Errors: INFEASIBLE (no pair passes Eq. (4)-(5)); OVERFLOW (a cost or makespan out of
  * range, from the device status); NCCL; CUDA; the argument errors of the calls above. */
 dflop_status dflop_search_plans(const dflop_cluster* cl, const dflop_cost_model* cm, const dflop_mem_model* mm,

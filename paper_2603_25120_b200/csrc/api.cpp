@@ -27,6 +27,7 @@ namespace dflop {
 
 static thread_local std::string g_err;
 static void release_streams();
+static void release_config_tables();
 
 void set_error(const char* fmt, ...) {
     char buf[512];
@@ -199,6 +200,7 @@ const char* dflop_last_error(void) { return g_err.c_str(); }
 dflop_status dflop_release_caches(void) {
     release_slot_programs();
     release_streams();
+    release_config_tables();
     return DFLOP_OK;
 }
 
@@ -379,6 +381,15 @@ struct ConfigTable {
 static std::mutex g_cfg_mu;
 static std::map<std::tuple<int, uint32_t, uint32_t, uint32_t>, ConfigTable> g_cfg_cache;
 
+static void release_config_tables() {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    for (auto& kv : g_cfg_cache) {
+        if (kv.second.d_cfgs) cudaFree(kv.second.d_cfgs);
+        if (kv.second.d_pair_start) cudaFree(kv.second.d_pair_start);
+    }
+    g_cfg_cache.clear();
+}
+
 // Algorithm 1 phase 1: FindCombs in ascending (tp, pp); cartesian product per
 // split of N_gpus (R16).
 static void find_combs(uint32_t g, uint32_t node, std::vector<uint32_t>& out) {
@@ -433,7 +444,11 @@ static dflop_status get_config_table(uint32_t n_gpus, uint32_t node, uint32_t gb
         ce = cudaMemcpy(t.d_cfgs, t.cfgs.data(), t.cfgs.size() * 4, cudaMemcpyHostToDevice);
     if (ce == cudaSuccess)
         ce = cudaMemcpy(t.d_pair_start, t.pair_start.data(), t.pair_start.size() * 4, cudaMemcpyHostToDevice);
-    if (ce != cudaSuccess) return cuda_status(ce, "config table upload");
+    if (ce != cudaSuccess) {  // free a partial upload
+        if (t.d_cfgs) cudaFree(t.d_cfgs);
+        if (t.d_pair_start) cudaFree(t.d_pair_start);
+        return cuda_status(ce, "config table upload");
+    }
     auto res = g_cfg_cache.emplace(key, std::move(t));
     *out = &res.first->second;
     return DFLOP_OK;
@@ -702,7 +717,11 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
         for (uint32_t b = 0; b < D; ++b) {
             const uint32_t q = p * D + b, o = off[b] - off[0], nb = off[b + 1] - off[b];
             cudaStream_t sq = ss[q % ns];
-            if (cb >= cend) {
+            // an Algorithm-1 plan beyond the balancer's limits (S = E_pp + L_pp > 32, or
+            // m = N_mb * L_dp > 65535: possible at >= 34 GPUs) is not balanced: its results say
+            // "no candidate", so dflop_select_plan never picks it (include/dflop.h)
+            const bool over = plans[p].e_pp + plans[p].l_pp > 32 || (uint64_t)plans[p].n_mb * plans[p].l_dp > 65535u;
+            if (cb >= cend || over) {
                 // empty shard on this rank: mark the (plan, batch) result as "no candidate"
                 ce = cudaMemsetAsync(&results[q], 0xFF, sizeof(dflop_cand_result), sq);
                 if (ce != cudaSuccess) return cuda_status(ce, "memset");
@@ -910,8 +929,10 @@ extern "C" dflop_status dflop_exact_cmax(const uint32_t* cost_ticks, uint32_t n,
     g_err.clear();
     dflop_status st = validate_plan(plan);
     if (st != DFLOP_OK) return st;
-    const uint32_t m = plan->n_mb * plan->l_dp;
-    if (m > 256) return invalid("exact solver: m = %u > 256", m);
+    if (plan->n_mb > 65535 || plan->l_dp > 65535) return invalid("exact solver: n_mb or l_dp > 65535");
+    const uint64_t m64 = (uint64_t)plan->n_mb * plan->l_dp;
+    if (m64 > 256) return invalid("exact solver: m = %llu > 256", (unsigned long long)m64);
+    const uint32_t m = (uint32_t)m64;
     if (plan->e_pp + plan->l_pp > 32) return invalid("S = E_pp + L_pp must be <= 32");
     if (n > 65535) {
         set_error("n=%u > 65535", n);

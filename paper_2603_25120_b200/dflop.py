@@ -240,6 +240,19 @@ def _u32(t):
     return t
 
 
+def _ticks(t):
+    """[4][n] u32 cost ticks (int32/uint32, CUDA, contiguous: the C side reads rows n apart)."""
+    _u32(t)
+    assert t.dim() == 2 and t.shape[0] == 4, tuple(t.shape)
+    return t
+
+
+def _u64(t):
+    import torch
+    assert t.dtype in (torch.int64, torch.uint64) and t.is_cuda and t.is_contiguous(), t.dtype
+    return t
+
+
 # ---------------------------------------------------------------- API (same names as the C ABI)
 # ---------------------------------------------------------------- sharding protocol (host)
 def shard_range(K: int, rank: int, world: int):
@@ -323,7 +336,7 @@ def balance_microbatches(cost_ticks, plan: Dict, K: int, R: int, G: int, seed: S
                          ws: Optional[Workspace] = None, stream=None):
     """a2-a5 for one plan; returns dict with 'best' (CandResult tensor view), 'assign', 'groups', 'cand_T', ..."""
     import torch
-    n = cost_ticks.shape[1]
+    n = _ticks(cost_ticks).shape[1]
     dev = cost_ticks.device
     c_end = K if c_end is None else c_end
     bp = BalanceParams()
@@ -363,6 +376,8 @@ def cand_result(best_tensor) -> Dict:
 def simulate_1f1b(fwd, bwd, want_busy: bool = True, stream=None):
     """fwd, bwd: int64 [C][S][M] (u64 ticks) -> (makespan [C], busy [C][S] or None)."""
     import torch
+    _u64(fwd), _u64(bwd)
+    assert fwd.shape == bwd.shape and fwd.dim() == 3, (tuple(fwd.shape), tuple(bwd.shape))
     Cn, S, M = fwd.shape
     out = torch.empty(Cn, dtype=torch.int64, device=fwd.device)
     busy = torch.empty((Cn, S), dtype=torch.int64, device=fwd.device) if want_busy else None
@@ -433,7 +448,7 @@ def exact_cmax(cost_ticks, plan: Dict, node_budget: int = 10 ** 9, init_assign=N
     """N3: exact C_max by branch and bound (synchronous).  Returns the dflop_exact_result
     fields and 'assign' (device int32 [n])."""
     import torch
-    n = cost_ticks.shape[1]
+    n = _ticks(cost_ticks).shape[1]
     dev = cost_ticks.device
     ps = plan_struct(plan)
     L = lib()
@@ -445,7 +460,7 @@ def exact_cmax(cost_ticks, plan: Dict, node_budget: int = 10 ** 9, init_assign=N
     have = C.c_size_t(wsb.numel())
     assign = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     _check(L.dflop_exact_cmax(_ptr(cost_ticks), n, C.byref(ps), C.c_uint64(int(node_budget)),
-                              _ptr(init_assign) if init_assign is not None else None, _ptr(wsb), C.byref(have),
+                              _ptr(_u32(init_assign)) if init_assign is not None else None, _ptr(wsb), C.byref(have),
                               C.byref(out), _ptr(assign), _stream(stream)))
     r = {f: getattr(out, f) for f, _ in ExactResult._fields_ if f not in ("struct_size", "reserved")}
     r["proven"] = bool(r["proven"])
@@ -458,19 +473,19 @@ def order_search(cost_ticks, plan: Dict, assign, rounds: int = 64, ws: Optional[
                  stream=None) -> Dict:
     """N4(a): per replica the improved slot order (bucket per slot) and its 1F1B makespan."""
     import torch
-    n = cost_ticks.shape[1]
+    n = _ticks(cost_ticks).shape[1]
     dev = cost_ticks.device
     ps = plan_struct(plan)
     L = lib()
     need = C.c_size_t(0)
-    _check(L.dflop_order_search(_ptr(cost_ticks), n, C.byref(ps), _ptr(assign), rounds, None, C.byref(need), None,
+    _check(L.dflop_order_search(_ptr(cost_ticks), n, C.byref(ps), _ptr(_u32(assign)), rounds, None, C.byref(need), None,
                                 None, None))
     wsb = (ws or _default_ws).get(need.value, dev)
     have = C.c_size_t(wsb.numel())
     M, rep = int(plan["n_mb"]), int(plan["l_dp"])
     order = torch.empty(rep * M, dtype=torch.int32, device=dev)
     T = np.zeros(rep, np.uint64)
-    _check(L.dflop_order_search(_ptr(cost_ticks), n, C.byref(ps), _ptr(assign), rounds, _ptr(wsb), C.byref(have),
+    _check(L.dflop_order_search(_ptr(cost_ticks), n, C.byref(ps), _ptr(_u32(assign)), rounds, _ptr(wsb), C.byref(have),
                                 _ptr(order), T.ctypes.data_as(C.c_void_p), _stream(stream)))
     return dict(order=order.view(rep, M), T=T, makespan=int(T.max()) if rep else 0)
 
@@ -478,12 +493,12 @@ def order_search(cost_ticks, plan: Dict, assign, rounds: int = 64, ws: Optional[
 def route_plan(cost_ticks, plan: Dict, assign, ws: Optional[Workspace] = None, stream=None) -> Dict:
     """N4(b): the inter-model communicator's routing plan (device tensors)."""
     import torch
-    n = cost_ticks.shape[1]
+    n = _ticks(cost_ticks).shape[1]
     dev = cost_ticks.device
     ps = plan_struct(plan)
     L = lib()
     need = C.c_size_t(0)
-    _check(L.dflop_route_plan(_ptr(cost_ticks), n, C.byref(ps), _ptr(assign), None, C.byref(need), None, None, None,
+    _check(L.dflop_route_plan(_ptr(cost_ticks), n, C.byref(ps), _ptr(_u32(assign)), None, C.byref(need), None, None, None,
                               None, None, None))
     wsb = (ws or _default_ws).get(need.value, dev)
     have = C.c_size_t(wsb.numel())
@@ -493,7 +508,7 @@ def route_plan(cost_ticks, plan: Dict, assign, ws: Optional[Workspace] = None, s
     eo = torch.empty(M * (G + 1), dtype=torch.int32, device=dev)
     lo = torch.empty(M * (R + 1), dtype=torch.int32, device=dev)
     el = torch.empty(M * G, dtype=torch.int64, device=dev)
-    _check(L.dflop_route_plan(_ptr(cost_ticks), n, C.byref(ps), _ptr(assign), _ptr(wsb), C.byref(have), _ptr(pos),
+    _check(L.dflop_route_plan(_ptr(cost_ticks), n, C.byref(ps), _ptr(_u32(assign)), _ptr(wsb), C.byref(have), _ptr(pos),
                               _ptr(so), _ptr(eo), _ptr(lo), _ptr(el), _stream(stream)))
     return dict(pos_item=pos[:n], slot_off=so, enc_off=eo.view(M, G + 1), llm_off=lo.view(M, R + 1),
                 enc_load=el.view(M, G))
