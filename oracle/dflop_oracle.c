@@ -143,6 +143,52 @@ uint32_t orc_shape_bin(uint64_t x) {
     return q < ORC_CORR_BINS ? q : ORC_CORR_BINS - 1;
 }
 
+/* ---------------------------------------------------------------- N1 tracker */
+int orc_tracker_init(orc_tracker* t, double alpha, uint32_t window, double cost) {
+    if (!(alpha > 0.0 && alpha <= 1.0) || window < 1 || window > ORC_TRACK_WIN) return ORC_INVALID;
+    memset(t, 0, sizeof *t);
+    t->alpha = alpha;
+    t->window = window;
+    t->cost = cost;
+    t->active = 1;
+    return ORC_OK;
+}
+
+/* S:420 record_observation: exponential average of Th_actual per shape bucket; S:421 the
+ * deviation B = Th_actual - Th_pred of the bucket (Eq. (6)). */
+double orc_tracker_record(orc_tracker* t, uint32_t grid, uint64_t x, double th_actual, double th_pred) {
+    uint32_t q = orc_shape_bin(x);
+    if (t->seen[grid][q])
+        t->observed[grid][q] = (1.0 - t->alpha) * t->observed[grid][q] + t->alpha * th_actual;
+    else {
+        t->observed[grid][q] = th_actual;
+        t->seen[grid][q] = 1;
+    }
+    t->predicted[grid][q] = th_pred;
+    return t->observed[grid][q] - t->predicted[grid][q];
+}
+
+void orc_tracker_rho(const orc_tracker* t, double* rho) {
+    for (uint32_t g = 0; g < 3; g++)
+        for (uint32_t q = 0; q < ORC_CORR_BINS; q++)
+            rho[g * ORC_CORR_BINS + q] = t->seen[g][q] ? t->observed[g][q] / t->predicted[g][q] : 1.0;
+}
+
+/* S:431 cost_benefit_step: deactivate when the average benefit of the last I
+ * iterations does not exceed the recurring cost C; never reactivated. */
+uint32_t orc_tracker_cost_benefit(orc_tracker* t, const double* benefits, uint32_t nb) {
+    for (uint32_t i = 0; i < nb; i++) {
+        t->last[t->n_benefits % ORC_TRACK_WIN] = benefits[i];
+        t->n_benefits++;
+    }
+    if (t->active && t->n_benefits >= t->window) {
+        double sum = 0.0;
+        for (uint32_t i = 0; i < t->window; i++) sum += t->last[(t->n_benefits - 1 - i) % ORC_TRACK_WIN];
+        t->active = (sum / (double)t->window) > t->cost;
+    }
+    return t->active;
+}
+
 int orc_predict(const orc_model* m, const orc_plan* p, const uint32_t* tiles, const uint32_t* frames,
                 const uint32_t* text, uint32_t n, double* cost_f64, uint32_t* cost_q, uint32_t* bad) {
     return orc_predict_corrected(m, p, tiles, frames, text, n, NULL, cost_f64, cost_q, bad);

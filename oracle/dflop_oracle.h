@@ -116,6 +116,28 @@ int orc_predict_corrected(const orc_model* m, const orc_plan* p, const uint32_t*
                           const uint32_t* text, uint32_t n, const double* rho, double* cost_f64, uint32_t* cost_q,
                           uint32_t* bad);
 
+/* N1 tracker, written from SPEC's operations:
+ *   record_observation(grid, x, Th_actual, Th_pred): the bucket (grid, orc_shape_bin(x))
+ *     keeps the exponential average of the observed throughput (weight alpha; the first
+ *     observation initialises it, R32) and the latest prediction; returns the bucket's
+ *     deviation B = Th_actual_avg - Th_pred (Eq. (6)).
+ *   rho[g][q] = Th_actual_avg / Th_pred of a recorded bucket, 1 otherwise (R31).
+ *   cost_benefit(benefits): appends the realised benefits; while active and at least I
+ *     benefits are known, active <- (mean of the last I) > C; off is permanent. */
+#define ORC_TRACK_WIN 4096
+typedef struct orc_tracker {
+    double alpha, cost;
+    uint32_t window, active;
+    double observed[3][ORC_CORR_BINS], predicted[3][ORC_CORR_BINS];
+    uint8_t seen[3][ORC_CORR_BINS];
+    uint64_t n_benefits;                 /* benefits appended so far      */
+    double last[ORC_TRACK_WIN];          /* ring of the latest benefits   */
+} orc_tracker;
+int orc_tracker_init(orc_tracker* t, double alpha, uint32_t window, double cost);
+double orc_tracker_record(orc_tracker* t, uint32_t grid, uint64_t x, double th_actual, double th_pred);
+void orc_tracker_rho(const orc_tracker* t, double* rho /* [3][ORC_CORR_BINS] */);
+uint32_t orc_tracker_cost_benefit(orc_tracker* t, const double* benefits, uint32_t nb);
+
 /* Step a2: base order pi: key max(e_i, l_i) descending, index ascending. */
 void orc_base_order(const uint32_t* cost_q, uint32_t n, uint32_t* order);
 

@@ -57,6 +57,16 @@ class OrcMem(C.Structure):
                 ("mem_per_gpu", C.c_double)]
 
 
+CORR_BINS, TRACK_WIN = 32, 4096
+
+
+class OrcTracker(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("cost", C.c_double), ("window", C.c_uint32), ("active", C.c_uint32),
+                ("observed", (C.c_double * CORR_BINS) * 3), ("predicted", (C.c_double * CORR_BINS) * 3),
+                ("seen", (C.c_uint8 * CORR_BINS) * 3), ("n_benefits", C.c_uint64),
+                ("last", C.c_double * TRACK_WIN)]
+
+
 class OrcPlan(C.Structure):
     _fields_ = [(k, C.c_uint32) for k in ("e_tp", "e_pp", "e_dp", "l_tp", "l_pp", "l_dp", "n_mb")]
 
@@ -132,6 +142,12 @@ def load(path: str):
         L.orc_stage_a_all.restype = C.c_uint64
         L.orc_stage_a_top.argtypes = [u64p, C.c_uint64, C.c_uint32, u64p]
         L.orc_stage_a_top.restype = C.c_uint32
+    L.orc_tracker_init.argtypes = [P(OrcTracker), C.c_double, C.c_uint32, C.c_double]
+    L.orc_tracker_record.argtypes = [P(OrcTracker), C.c_uint32, C.c_uint64, C.c_double, C.c_double]
+    L.orc_tracker_record.restype = C.c_double
+    L.orc_tracker_rho.argtypes = [P(OrcTracker), f64p]
+    L.orc_tracker_cost_benefit.argtypes = [P(OrcTracker), f64p, C.c_uint32]
+    L.orc_tracker_cost_benefit.restype = C.c_uint32
     return L
 
 
@@ -238,6 +254,26 @@ def predict(model: Dict, plan: Dict, tiles, frames, text):
 
 
 CORR_BINS = 32
+
+
+class Tracker:
+    """The oracle's N1 tracker (orc_tracker_*)."""
+
+    def __init__(self, alpha=0.25, window=10, cost=0.0):
+        self.s = OrcTracker()
+        assert lib().orc_tracker_init(C.byref(self.s), alpha, window, cost) == 0
+
+    def record(self, grid: int, x: int, th_actual: float, th_pred: float) -> float:
+        return lib().orc_tracker_record(C.byref(self.s), grid, int(x), th_actual, th_pred)
+
+    def rho(self):
+        r = np.zeros((3, CORR_BINS))
+        lib().orc_tracker_rho(C.byref(self.s), _p(r, C.c_double))
+        return r
+
+    def cost_benefit(self, benefits) -> bool:
+        b = np.ascontiguousarray(np.asarray(list(benefits), dtype=np.float64))
+        return bool(lib().orc_tracker_cost_benefit(C.byref(self.s), _p(b, C.c_double) if b.size else None, b.size))
 
 
 def shape_bin(x: int) -> int:
