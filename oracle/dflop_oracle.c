@@ -624,6 +624,109 @@ int orc_exact_cmax(const uint32_t* q, uint32_t n, uint32_t m, uint64_t node_budg
 }
 
 /* ------------------------------------------------------------------------- */
+/* N3 for m = 2 and m = 4: exact C_max by pair decomposition (see the header).  */
+/* Subsets are visited in Gray-code order (one element toggled per step), the   */
+/* set sums updated by +/- that element; every subset is visited exactly once.  */
+/* ------------------------------------------------------------------------- */
+static uint32_t ctz64(uint64_t x) { uint32_t c = 0; while (!(x & 1ull)) { x >>= 1; c++; } return c; }
+
+/* the best 2-way split of the k items (e[], l[]): min over subsets Y that contain item 0 of
+ * max(E(Y), L(Y), E - E(Y), L - L(Y)); *best_y = a minimising subset (bit t = item t) */
+static uint64_t best_split2(const uint64_t* e, const uint64_t* l, uint32_t k, uint64_t* best_y) {
+    uint64_t SE = 0, SL = 0;
+    for (uint32_t t = 0; t < k; t++) { SE += e[t]; SL += l[t]; }
+    if (k == 0) { *best_y = 0; return 0; }
+    /* Y = {0} u (Gray subset of items 1..k-1) */
+    uint64_t y = 1ull, EY = e[0], LY = l[0];
+    uint64_t best = max64(max64(EY, LY), max64(SE - EY, SL - LY));
+    *best_y = y;
+    uint64_t steps = 1ull << (k - 1);
+    for (uint64_t i = 1; i < steps; i++) {
+        uint32_t b = 1 + ctz64(i);              /* Gray code: toggle element 1 + ctz(i) */
+        y ^= 1ull << b;
+        if (y & (1ull << b)) { EY += e[b]; LY += l[b]; } else { EY -= e[b]; LY -= l[b]; }
+        uint64_t v = max64(max64(EY, LY), max64(SE - EY, SL - LY));
+        if (v < best) { best = v; *best_y = y; }
+    }
+    return best;
+}
+
+int orc_exact_pairs(const uint32_t* q, uint32_t n, uint32_t m, const uint32_t* init_assign, uint32_t* assign_out,
+                    uint64_t* cmax, uint64_t* lower_bound, uint64_t* visited) {
+    if ((m != 2 && m != 4) || n < 1 || n > 40) return ORC_INVALID;
+    uint64_t e[40], l[40], SE = 0, SL = 0, big = 0;
+    for (uint32_t i = 0; i < n; i++) {
+        e[i] = item_e(q, n, i); l[i] = item_l(q, n, i);
+        SE += e[i]; SL += l[i]; big = max64(big, max64(e[i], l[i]));
+    }
+    *lower_bound = max64(max64((SE + m - 1) / m, (SL + m - 1) / m), big);
+    /* incumbent: the caller's assignment, else the paper's LPT (orc_exact_cmax's rule) */
+    uint64_t inc = 0, lb2 = 0, nodes = 0;
+    uint32_t proven = 0;
+    uint32_t* a0 = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    if (orc_exact_cmax(q, n, m, 0, init_assign, a0, &inc, &lb2, &proven, &nodes) != ORC_OK) { free(a0); return ORC_INVALID; }
+    uint64_t best = inc, bestX = 0, bestY1 = 0, bestY2 = 0, cnt = 0;
+    int found = 0;
+    if (m == 2) {
+        uint64_t y;
+        uint64_t v = best_split2(e, l, n, &y);
+        cnt = 1ull << (n - 1);
+        if (v < best) { best = v; bestX = y; found = 1; }
+    } else if (inc > 0) {
+        /* X = buckets {0, 1} (contains item 0), complement = buckets {2, 3}; a 4-way
+         * assignment of max C has E(X), L(X) in [S - 2C, 2C]; only X's that can beat the
+         * incumbent (C = inc - 1) are split */
+        /* the window follows the best value found so far (C0 = best - 1) */
+        uint64_t C0 = inc - 1;
+        uint64_t loE = SE > 2 * C0 ? SE - 2 * C0 : 0, loL = SL > 2 * C0 ? SL - 2 * C0 : 0;
+        uint64_t x = 1ull, EX = e[0], LX = l[0];
+        uint64_t steps = 1ull << (n - 1);
+        uint64_t ex[40], lx[40], ec[40], lc[40];
+        for (uint64_t i = 0; i < steps; i++) {
+            if (i > 0) {
+                uint32_t b = 1 + ctz64(i);
+                x ^= 1ull << b;
+                if (x & (1ull << b)) { EX += e[b]; LX += l[b]; } else { EX -= e[b]; LX -= l[b]; }
+            }
+            cnt++;
+            if (EX < loE || EX > 2 * C0 || LX < loL || LX > 2 * C0) continue;
+            uint32_t kx = 0, kc = 0;
+            for (uint32_t t = 0; t < n; t++) {
+                if (x & (1ull << t)) { ex[kx] = e[t]; lx[kx] = l[t]; kx++; }
+                else { ec[kc] = e[t]; lc[kc] = l[t]; kc++; }
+            }
+            uint64_t y1, y2;
+            uint64_t v1 = best_split2(ex, lx, kx, &y1);
+            if (v1 >= best) continue;
+            uint64_t v2 = best_split2(ec, lc, kc, &y2);
+            uint64_t v = max64(v1, v2);
+            if (v < best) {
+                best = v; bestX = x; bestY1 = y1; bestY2 = y2; found = 1;
+                if (best == 0) break;
+                C0 = best - 1;
+                loE = SE > 2 * C0 ? SE - 2 * C0 : 0;
+                loL = SL > 2 * C0 ? SL - 2 * C0 : 0;
+            }
+        }
+    }
+    *cmax = best;
+    *visited = cnt;
+    if (assign_out) {
+        if (!found) memcpy(assign_out, a0, sizeof(uint32_t) * n);
+        else if (m == 2) { for (uint32_t t = 0; t < n; t++) assign_out[t] = (bestX >> t) & 1ull ? 0u : 1u; }
+        else {
+            uint32_t kx = 0, kc = 0;
+            for (uint32_t t = 0; t < n; t++) {
+                if (bestX & (1ull << t)) { assign_out[t] = (bestY1 >> kx) & 1ull ? 0u : 1u; kx++; }
+                else { assign_out[t] = (bestY2 >> kc) & 1ull ? 2u : 3u; kc++; }
+            }
+        }
+    }
+    free(a0);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
 /* N4(a): microbatch-order search per replica (see the header).                */
 /* ------------------------------------------------------------------------- */
 static uint64_t order_makespan(const bucket_sums* bk, const orc_plan* p, uint32_t rho, const uint32_t* ord,

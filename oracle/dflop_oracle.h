@@ -168,6 +168,17 @@ int orc_exact_cmax(const uint32_t* cost_q, uint32_t n, uint32_t m, uint64_t node
                    const uint32_t* init_assign, uint32_t* assign_out, uint64_t* cmax, uint64_t* lower_bound,
                    uint32_t* proven, uint64_t* nodes);
 
+/* N3 certificate for m = 2 and m = 4 buckets (n <= 40): exact C_max by pair decomposition.
+ * m = 2: the minimum over subsets Y (item 0 in Y) of max(E(Y), L(Y), E - E(Y), L - L(Y)).
+ * m = 4: buckets {0, 1} form a set X (item 0 in X, by symmetry), {2, 3} its complement; the
+ * optimum is min over X of max(split2(X), split2(complement)), split2 = the m = 2 optimum of a
+ * set.  Every X whose sums E(X), L(X) lie in [S - 2C, 2C] for C = best value so far - 1 is split (no
+ * 4-way assignment with max < incumbent has X outside that window); exhaustive, so the result
+ * is the optimum (a certificate), the incumbent (init_assign's C_max or the paper's LPT) when
+ * nothing beats it.  visited = subsets X (m = 4) or Y (m = 2) enumerated. */
+int orc_exact_pairs(const uint32_t* cost_q, uint32_t n, uint32_t m, const uint32_t* init_assign, uint32_t* assign_out,
+                    uint64_t* cmax, uint64_t* lower_bound, uint64_t* visited);
+
 /* N4(a) microbatch-order search (R11: the 1F1B makespan depends on the slot order; SURVEY
  * 8(f) N4).  For each LLM replica rho (buckets j = k * L_dp + rho, slot k by default, R10)
  * independently: start from the best of four orders -- 0 identity, 1 ascending W_j =

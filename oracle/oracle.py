@@ -142,6 +142,7 @@ def load(path: str):
         L.orc_stage_a_all.restype = C.c_uint64
         L.orc_stage_a_top.argtypes = [u64p, C.c_uint64, C.c_uint32, u64p]
         L.orc_stage_a_top.restype = C.c_uint32
+    L.orc_exact_pairs.argtypes = [u32p, C.c_uint32, C.c_uint32, u32p, u32p, u64p, u64p, u64p]
     L.orc_tracker_init.argtypes = [P(OrcTracker), C.c_double, C.c_uint32, C.c_double]
     L.orc_tracker_record.argtypes = [P(OrcTracker), C.c_uint32, C.c_uint64, C.c_double, C.c_double]
     L.orc_tracker_record.restype = C.c_double
@@ -507,6 +508,19 @@ def exact_cmax(cost_q, m, node_budget=10 ** 7, init_assign=None):
     if st != 0:
         raise ValueError(f"orc_exact_cmax status {st}")
     return dict(cmax=int(cm[0]), lb=int(lb[0]), proven=bool(pr[0]), nodes=int(nodes[0]), assign=a[:n])
+
+
+def exact_pairs(cost_q, m, init_assign=None):
+    """N3 certificate by pair decomposition (m = 2 or 4, n <= 40): the optimum C_max."""
+    q = _u32(cost_q)
+    n = q.shape[1]
+    a = np.zeros(max(n, 1), np.uint32)
+    cm, lb, vis = np.zeros(1, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+    ia = None if init_assign is None else _u32(init_assign)
+    st = lib().orc_exact_pairs(_p(q, C.c_uint32), n, m, _p(ia, C.c_uint32) if ia is not None else None,
+                               _p(a, C.c_uint32), _p(cm, C.c_uint64), _p(lb, C.c_uint64), _p(vis, C.c_uint64))
+    assert st == 0, st
+    return dict(cmax=int(cm[0]), lb=int(lb[0]), visited=int(vis[0]), assign=a[:n])
 
 
 def order_search(cost_q, plan: Dict, assign, rounds=64):

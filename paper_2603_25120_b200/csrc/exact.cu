@@ -17,6 +17,16 @@
 //                   1F1B instances of its replicas (scored by k_simulate: the "extra
 //                   candidate" of SURVEY 8(f) N3)
 //
+// m = 2 and m = 4 with n <= kPDMaxN use an exhaustive pair decomposition instead of the tree
+// (k_pd_*: the same certificate as oracle/orc_exact_pairs, DESIGN.md section 10b N3):
+//   m = 2  every subset Y holding base position 0 (Gray-code enumeration over the GPU):
+//          C = max(E(Y), L(Y), E - E(Y), L - L(Y)), minimum over Y;
+//   m = 4  buckets {0, 1} form X (position 0 in X), {2, 3} its complement; X's with E(X),
+//          L(X) in [S - 2C0, 2C0] (C0 = incumbent - 1: no better assignment has X outside)
+//          are listed, then one warp per X computes the best 2-way splits of X and of its
+//          complement (Gray enumeration over the lanes); C = min over X of the larger one.
+//          A list overflow splits the first kPDCap X's, tightens C0 and re-enumerates.
+//
 // The optimum is unique as a value; the assignment returned is one optimal (or best found)
 // assignment.  Subtree search: n <= kExactMaxN, m <= 32; beyond that only the bound and the
 // initial incumbent are reported (proven iff they meet).
@@ -342,12 +352,253 @@ __global__ void k_exact_final(uint32_t n, uint32_t m, const uint32_t* __restrict
     }
 }
 
+// ---------------------------------------------------------------- pair decomposition (m = 2, 4)
+constexpr uint32_t kPDMaxN = 34;          // 2^33 subsets X at most
+constexpr uint32_t kPDCap = 1u << 20;     // listed X's per enumeration pass
+constexpr uint32_t kPDBlocks = 148 * 8, kPDThreads = 256;
+
+struct PDHdr {
+    unsigned long long best;   // (C << 24) | list index (m = 4) -- min over split X's
+    unsigned long long count;  // X's in the window this pass
+    u64 sum_e, sum_l;
+    u64 visited;
+};
+
+// sums of the subset `mask` of base positions
+DFLOP_DEV void pd_sums(const u64* pe, const u64* pl, uint32_t n, u64 mask, u64& E, u64& L) {
+    E = 0;
+    L = 0;
+    for (uint32_t t = 0; t < n; ++t)
+        if ((mask >> t) & 1ull) {
+            E += pe[t];
+            L += pl[t];
+        }
+}
+
+// every subset holding position 0, in Gray-code order: index i -> {0} u gray(i) shifted by 1;
+// m = 2: per-block minimum of (C(Y), Y) into blk[]; m = 4: X's in the window into list[]
+__global__ void __launch_bounds__(kPDThreads) k_pd_enum(uint32_t n, uint32_t m, const u64* __restrict__ pe,
+                                                         const u64* __restrict__ pl, u64 C0, u64* list,
+                                                         PDHdr* ph, u64* blk) {
+    __shared__ u64 sv[kPDThreads], sm[kPDThreads];
+    const u64 SE = ph->sum_e, SL = ph->sum_l;
+    const u64 loE = SE > 2 * C0 ? SE - 2 * C0 : 0, loL = SL > 2 * C0 ? SL - 2 * C0 : 0, hi = 2 * C0;
+    const u64 steps = 1ull << (n - 1);
+    const u64 nthr = (u64)gridDim.x * blockDim.x, tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    const u64 chunk = (steps + nthr - 1) / nthr;
+    const u64 i0 = tid * chunk, i1 = min(steps, i0 + chunk);
+    u64 bv = ~0ull, bm = 0;
+    if (i0 < i1) {
+        u64 x = 1ull | ((i0 ^ (i0 >> 1)) << 1);
+        u64 E, L;
+        pd_sums(pe, pl, n, x, E, L);
+        for (u64 i = i0; i < i1; ++i) {
+            if (i > i0) {
+                const uint32_t b = 1 + (uint32_t)__ffsll((long long)i) - 1;
+                x ^= 1ull << b;
+                if ((x >> b) & 1ull) {
+                    E += pe[b];
+                    L += pl[b];
+                } else {
+                    E -= pe[b];
+                    L -= pl[b];
+                }
+            }
+            if (m == 2) {
+                const u64 v = umax64(umax64(E, L), umax64(SE - E, SL - L));
+                if (v < bv) {
+                    bv = v;
+                    bm = x;
+                }
+            } else if (E >= loE && E <= hi && L >= loL && L <= hi) {
+                const unsigned long long k = atomicAdd(&ph->count, 1ull);
+                if (k < kPDCap) list[k] = x;
+            }
+        }
+    }
+    if (m == 2) {  // block minimum (value, mask)
+        sv[threadIdx.x] = bv;
+        sm[threadIdx.x] = bm;
+        __syncthreads();
+        for (uint32_t s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s && (sv[threadIdx.x + s] < sv[threadIdx.x] ||
+                                    (sv[threadIdx.x + s] == sv[threadIdx.x] && sm[threadIdx.x + s] < sm[threadIdx.x]))) {
+                sv[threadIdx.x] = sv[threadIdx.x + s];
+                sm[threadIdx.x] = sm[threadIdx.x + s];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            blk[2 * blockIdx.x] = sv[0];
+            blk[2 * blockIdx.x + 1] = sm[0];
+        }
+    }
+}
+
+// best 2-way split of the k items (e[], l[]) by the 32 lanes of a warp: subsets holding item 0,
+// lane chunks of the Gray sequence; returns (value, mask) of the lexicographic minimum
+DFLOP_DEV void pd_split_warp(const u64* e, const u64* l, uint32_t k, u64& best_v, u64& best_y) {
+    const uint32_t lane = threadIdx.x & 31u;
+    u64 SE = 0, SL = 0;
+    for (uint32_t t = 0; t < k; ++t) {
+        SE += e[t];
+        SL += l[t];
+    }
+    const u64 steps = k ? 1ull << (k - 1) : 0ull;
+    const u64 chunk = (steps + 31) / 32;
+    const u64 i0 = (u64)lane * chunk, i1 = min(steps, i0 + chunk);
+    u64 bv = ~0ull, by = 0;
+    if (i0 < i1) {
+        u64 y = 1ull | ((i0 ^ (i0 >> 1)) << 1);
+        u64 E = 0, L = 0;
+        for (uint32_t t = 0; t < k; ++t)
+            if ((y >> t) & 1ull) {
+                E += e[t];
+                L += l[t];
+            }
+        for (u64 i = i0; i < i1; ++i) {
+            if (i > i0) {
+                const uint32_t b = (uint32_t)__ffsll((long long)i);  // 1 + ctz(i)
+                y ^= 1ull << b;
+                if ((y >> b) & 1ull) {
+                    E += e[b];
+                    L += l[b];
+                } else {
+                    E -= e[b];
+                    L -= l[b];
+                }
+            }
+            const u64 v = umax64(umax64(E, L), umax64(SE - E, SL - L));
+            if (v < bv) {
+                bv = v;
+                by = y;
+            }
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const u64 v2 = __shfl_xor_sync(0xFFFFFFFFu, bv, off), y2 = __shfl_xor_sync(0xFFFFFFFFu, by, off);
+        if (v2 < bv || (v2 == bv && y2 < by)) {
+            bv = v2;
+            by = y2;
+        }
+    }
+    if (k == 0) bv = 0;
+    best_v = bv;
+    best_y = by;
+}
+
+// one warp per listed X: C(X) = max(split2(X), split2(complement)); atomicMin of (C << 24 | idx)
+__global__ void __launch_bounds__(128) k_pd_split(uint32_t n, const u64* __restrict__ pe, const u64* __restrict__ pl,
+                                                  const u64* __restrict__ list, uint32_t count, u64 inc, PDHdr* ph) {
+    __shared__ u64 se[4][2][kPDMaxN], sl[4][2][kPDMaxN];
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t x = blockIdx.x * (blockDim.x >> 5) + w; x < count; x += warps) {
+        const u64 mask = list[x];
+        if (lane == 0) {
+            uint32_t a = 0, b = 0;
+            for (uint32_t t = 0; t < n; ++t) {
+                if ((mask >> t) & 1ull) {
+                    se[w][0][a] = pe[t];
+                    sl[w][0][a++] = pl[t];
+                } else {
+                    se[w][1][b] = pe[t];
+                    sl[w][1][b++] = pl[t];
+                }
+            }
+        }
+        __syncwarp();
+        const uint32_t kx = (uint32_t)__popcll(mask), kc = n - kx;
+        u64 v1, y1;
+        pd_split_warp(se[w][0], sl[w][0], kx, v1, y1);
+        const u64 cur = umax64(0, min(ph->best >> 24, inc));  // to beat: the best so far and the incumbent
+        if (v1 < cur) {  // warp-uniform (v1 reduced)
+            u64 v2, y2;
+            pd_split_warp(se[w][1], sl[w][1], kc, v2, y2);
+            const u64 v = umax64(v1, v2);
+            if (lane == 0 && v < cur) atomicMin(&ph->best, (v << 24) | x);
+        }
+        __syncwarp();
+    }
+}
+
+// the winner: m = 2 from the block minima, m = 4 from the best listed X (its splits recomputed);
+// writes best_by_item and the incumbent key when it beats the initial assignment
+__global__ void k_pd_final(uint32_t n, uint32_t m, const u64* __restrict__ pe, const u64* __restrict__ pl,
+                           const uint32_t* __restrict__ order, const u64* __restrict__ list, const u64* __restrict__ blk,
+                           uint32_t nblk, PDHdr* ph, uint32_t* best_by_item, ExactHdr* h) {
+    __shared__ u64 se[2][kPDMaxN], sl[2][kPDMaxN];
+    __shared__ u64 s_v, s_x, s_y1, s_y2;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (threadIdx.x >= 32) return;
+    if (m == 2) {
+        u64 bv = ~0ull, bm = 0;
+        for (uint32_t b = lane; b < nblk; b += 32)
+            if (blk[2 * b] < bv || (blk[2 * b] == bv && blk[2 * b + 1] < bm)) {
+                bv = blk[2 * b];
+                bm = blk[2 * b + 1];
+            }
+        for (int off = 16; off > 0; off >>= 1) {
+            const u64 v2 = __shfl_xor_sync(0xFFFFFFFFu, bv, off), m2 = __shfl_xor_sync(0xFFFFFFFFu, bm, off);
+            if (v2 < bv || (v2 == bv && m2 < bm)) {
+                bv = v2;
+                bm = m2;
+            }
+        }
+        if ((bv << 24) >> 24 == bv && bv < (h->key >> 24)) {
+            for (uint32_t t = lane; t < n; t += 32) best_by_item[order[t]] = ((bm >> t) & 1ull) ? 0u : 1u;
+            if (lane == 0) h->key = (bv << 24) | kOwnerInit;
+        }
+        return;
+    }
+    const unsigned long long key = ph->best;
+    if ((key >> 24) >= (h->key >> 24)) return;  // nothing beat the incumbent
+    const u64 mask = list[key & 0xFFFFFFull];
+    if (lane == 0) {
+        uint32_t a = 0, b = 0;
+        for (uint32_t t = 0; t < n; ++t) {
+            if ((mask >> t) & 1ull) {
+                se[0][a] = pe[t];
+                sl[0][a++] = pl[t];
+            } else {
+                se[1][b] = pe[t];
+                sl[1][b++] = pl[t];
+            }
+        }
+    }
+    __syncwarp();
+    const uint32_t kx = (uint32_t)__popcll(mask), kc = n - kx;
+    u64 v1, y1, v2, y2;
+    pd_split_warp(se[0], sl[0], kx, v1, y1);
+    pd_split_warp(se[1], sl[1], kc, v2, y2);
+    if (lane == 0) {
+        s_v = umax64(v1, v2);
+        s_x = mask;
+        s_y1 = y1;
+        s_y2 = y2;
+    }
+    __syncwarp();
+    // positions of X in increasing order are X's items 0..kx-1 (same for the complement)
+    if (lane == 0) {
+        uint32_t a = 0, b = 0;
+        for (uint32_t t = 0; t < n; ++t) {
+            if ((s_x >> t) & 1ull)
+                best_by_item[order[t]] = ((s_y1 >> a++) & 1ull) ? 0u : 1u;
+            else
+                best_by_item[order[t]] = ((s_y2 >> b++) & 1ull) ? 2u : 3u;
+        }
+        h->key = (s_v << 24) | kOwnerInit;
+    }
+}
+
 size_t exact_ws_bytes(uint32_t n, uint32_t m, const dflop_plan* p) {
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t inst = (size_t)p->l_dp * (p->e_pp + p->l_pp) * p->n_mb;
+    const bool pd = (m == 2 || m == 4) && n >= 1 && n <= kPDMaxN;
     return al(sizeof(ExactHdr)) + al((size_t)n * 8) + al((size_t)n * 4) * 2 + al((size_t)n * 8) * 2 + al((size_t)kExactFront * kExactMaxN) +
            2 * al((size_t)kExactFront * sizeof(ExactNode)) + al((size_t)4 * m * 8) + 2 * al(inst * 8) +
-           al((size_t)p->l_dp * 8) + al(sizeof(BalanceHeader));
+           al((size_t)p->l_dp * 8) + al(sizeof(BalanceHeader)) +
+           (pd ? al(sizeof(PDHdr)) + al((size_t)kPDCap * 8) + al((size_t)kPDBlocks * 16) : 0);
 }
 
 dflop_status exact_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p, uint64_t node_budget,
@@ -371,8 +622,9 @@ dflop_status exact_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p,
     u64* fwd = reinterpret_cast<u64*>(w + o);                o += al(inst * 8);
     u64* bwd = reinterpret_cast<u64*>(w + o);                o += al(inst * 8);
     u64* ms = reinterpret_cast<u64*>(w + o);                 o += al((size_t)p->l_dp * 8);
-    BalanceHeader* bh = reinterpret_cast<BalanceHeader*>(w + o);
+    BalanceHeader* bh = reinterpret_cast<BalanceHeader*>(w + o); o += al(sizeof(BalanceHeader));
     uint32_t* item_pos = by_item;  // scratch for the rank sort (overwritten by k_exact_init)
+    bool h_pd_incomplete = false;
     cudaError_t ce = cudaMemsetAsync(bh, 0, sizeof(BalanceHeader), s);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(h, 0, sizeof(ExactHdr), s);
     if (ce != cudaSuccess) return cuda_status(ce, "memset");
@@ -384,7 +636,61 @@ dflop_status exact_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p,
     }
     k_exact_init<<<1, 256, 0, s>>>(cost, n, m, order, init_assign, pe, pl, by_item, h);
     count_launches(1);
-    const bool dfs = n > 0 && n <= kExactMaxN && m <= kExactMaxM;
+    // m = 2, 4 and small n: the exhaustive pair decomposition (a certificate) when its 2^(n-1)
+    // subsets fit the node budget; otherwise the tree search
+    const bool pd = (m == 2 || m == 4) && n >= 1 && n <= kPDMaxN && (1ull << (n - 1)) <= node_budget;
+    const bool dfs = !pd && n > 0 && n <= kExactMaxN && m <= kExactMaxM;
+    u64 pd_visited = 0;
+    if (pd) {
+        PDHdr* ph = reinterpret_cast<PDHdr*>(w + o);       o += al(sizeof(PDHdr));
+        u64* list = reinterpret_cast<u64*>(w + o);          o += al((size_t)kPDCap * 8);
+        u64* blk = reinterpret_cast<u64*>(w + o);           o += al((size_t)kPDBlocks * 16);
+        ExactHdr hh;
+        ce = cudaMemcpyAsync(&hh, h, sizeof hh, cudaMemcpyDeviceToHost, s);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+        if (ce != cudaSuccess) return cuda_status(ce, "exact init readback");
+        PDHdr p0;
+        memset(&p0, 0, sizeof p0);
+        p0.sum_e = hh.sum_e;
+        p0.sum_l = hh.sum_l;
+        u64 inc = hh.key >> 24;
+        p0.best = ~0ull;
+        for (int pass = 0; inc > hh.lb && pass < 64; ++pass) {
+            p0.count = 0;
+            ce = cudaMemcpyAsync(ph, &p0, sizeof p0, cudaMemcpyHostToDevice, s);
+            if (ce != cudaSuccess) return cuda_status(ce, "pd header");
+            k_pd_enum<<<kPDBlocks, kPDThreads, 0, s>>>(n, m, pe, pl, inc - 1, list, ph, blk);
+            count_launches(1);
+            pd_visited += 1ull << (n - 1);
+            if (m == 2) break;
+            unsigned long long cnt = 0;
+            ce = cudaMemcpyAsync(&cnt, &ph->count, 8, cudaMemcpyDeviceToHost, s);
+            if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+            if (ce != cudaSuccess) return cuda_status(ce, "pd count");
+            const uint32_t nx = (uint32_t)std::min<unsigned long long>(cnt, kPDCap);
+            if (nx > 0) {
+                k_pd_split<<<std::min<uint32_t>((nx + 3) / 4, 148 * 16), 128, 0, s>>>(n, pe, pl, list, nx, inc, ph);
+                k_pd_final<<<1, 32, 0, s>>>(n, m, pe, pl, order, list, blk, kPDBlocks, ph, by_item, h);
+                count_launches(2);
+            }
+            if (cnt <= kPDCap) break;
+            // overflow: the split X's tightened the incumbent; enumerate again with it
+            ce = cudaMemcpyAsync(&hh, h, sizeof hh, cudaMemcpyDeviceToHost, s);
+            if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+            if (ce != cudaSuccess) return cuda_status(ce, "pd readback");
+            const u64 inc2 = hh.key >> 24;
+            if (inc2 >= inc) {  // no progress with the first kPDCap X's: give up (not proven)
+                h_pd_incomplete = true;
+                break;
+            }
+            inc = inc2;
+            p0.best = ~0ull;
+        }
+        if (m == 2 && inc > hh.lb) {
+            k_pd_final<<<1, 32, 0, s>>>(n, m, pe, pl, order, list, blk, kPDBlocks, ph, by_item, h);
+            count_launches(1);
+        }
+    }
     if (dfs) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -417,9 +723,9 @@ dflop_status exact_launch(const uint32_t* cost, uint32_t n, const dflop_plan* p,
     r.struct_size = sizeof r;
     r.cmax = hh.key >> 24;
     r.lower_bound = hh.lb;
-    r.nodes = hh.nodes;
-    r.proven = (r.cmax <= hh.lb || (dfs && !hh.out_of_budget)) ? 1u : 0u;
-    r.searched = dfs ? 1u : 0u;
+    r.nodes = pd ? pd_visited : hh.nodes;
+    r.proven = (r.cmax <= hh.lb || (dfs && !hh.out_of_budget) || (pd && !h_pd_incomplete)) ? 1u : 0u;
+    r.searched = (dfs || pd) ? 1u : 0u;
     for (u64 v : hm) r.makespan = std::max<u64>(r.makespan, v);
     *out = r;
     return DFLOP_OK;

@@ -59,8 +59,48 @@ def test_medium_instances_vs_oracle(D, O, n, m, seed):
     assert BF.cmax_of(host_u32(g["assign"]), c, m) == g["cmax"]
 
 
+@pytest.mark.parametrize("m", [2, 4])
+def test_pair_decomposition_vs_oracle(D, O, m):
+    """m = 2, 4: the GPU's exhaustive pair decomposition equals the oracle's (orc_exact_pairs)
+    and brute force; proven."""
+    rng = np.random.default_rng(100 + m)
+    for trial in range(12):
+        n = int(rng.integers(1, 9)) if trial < 8 else int(rng.integers(12, 25))
+        c = rng.integers(0, 60 if trial < 8 else 50_000, (4, n)).astype(np.uint32)
+        g = D.exact_cmax(dev_u32(c), plan(m), node_budget=1 << 40)
+        o = O.exact_pairs(c, m)
+        assert g["proven"] and g["cmax"] == o["cmax"], (trial, n, g, o["cmax"])
+        if n <= 8:
+            assert g["cmax"] == BF.opt_cmax_2d(c, m)
+        a = host_u32(g["assign"])
+        assert BF.cmax_of(a, c, m) == g["cmax"] and g["lower_bound"] == o["lb"]
+
+
+def test_config1_certificate(D, O, presets):
+    """N3 certificate for config 1 (n = 32, m = 4): the pair decomposition proves
+    the optimum C_max of batch 0 -- the oracle's exhaustive decomposition gives the same value
+    -- and the returned assignment attains it."""
+    p = presets[1]
+    _, ticks = D.predict_costs(p.model, p.plan, *(dev_u32(a) for a in p.features(0)), want_f32=False)
+    q = host_u32(ticks).reshape(4, -1)
+    g = D.exact_cmax(ticks, p.plan, node_budget=1 << 40)
+    assert g["proven"] == 1
+    o = O.exact_pairs(q, 4)
+    assert g["cmax"] == o["cmax"] and g["lower_bound"] == o["lb"]
+    a = host_u32(g["assign"])
+    assert BF.cmax_of(a, q, 4) == g["cmax"]
+    T, cm = BF.score_assignment(a, q, p.plan)
+    assert g["makespan"] == T
+    # warm start from the search winner: the same certified optimum
+    t, f, x = (dev_u32(v) for v in p.features(0))
+    res = D.search_plans(p.model, t, f, x, K=65536, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan)
+    g2 = D.exact_cmax(ticks, p.plan, node_budget=1 << 40, init_assign=res["assign"])
+    assert g2["proven"] and g2["cmax"] == g["cmax"] <= res["cmax"]
+
+
 def test_presets_certificate(D, O, presets):
-    # config 1 (n = 32, m = 4): proven or a gap certificate; config 3: LB meets the LPT
+    # tree search within a node budget: config 1 (n = 32, m = 4) below the pair decomposition's
+    # 2^31 subsets is a gap certificate; config 3: LB meets the LPT
     for k in (1, 3):
         p = presets[k]
         _, ticks = D.predict_costs(p.model, p.plan, *(dev_u32(a) for a in p.features(0)), want_f32=False)

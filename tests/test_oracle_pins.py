@@ -614,6 +614,27 @@ def test_exact_budget_and_incumbent(O):
     assert full["proven"] and full["cmax"] == opt
 
 
+def test_exact_pairs_spec_examples_and_bruteforce(O):
+    """N3 pair decomposition (m = 2, 4): SPEC's examples, brute force over all m^n
+    assignments of random 2-D instances, and the branch and bound's proven optima."""
+    assert O.exact_pairs(loads_1d([8, 7, 6, 5, 4]), 2)["cmax"] == 15          # S:394
+    assert O.exact_pairs(loads_1d([3, 3, 2, 2, 2]), 2)["cmax"] == 6           # Graham-tight optimum
+    assert O.exact_pairs(loads_1d([6, 6]), 2)["cmax"] == 6                     # S:396
+    rng = np.random.default_rng(44)
+    for trial in range(60):
+        n, m = int(rng.integers(1, 9)), int(rng.choice([2, 4]))
+        c = rng.integers(0, 40, (4, n)).astype(np.uint32)
+        r = O.exact_pairs(c, m)
+        assert r["cmax"] == BF.opt_cmax_2d(c, m), (trial, n, m)
+        assert BF.cmax_of(r["assign"], c, m) == r["cmax"] and r["lb"] <= r["cmax"]
+    for trial in range(8):
+        n, m = int(rng.integers(10, 17)), int(rng.choice([2, 4]))
+        c = rng.integers(1, 5000, (4, n)).astype(np.uint32)
+        b = O.exact_cmax(c, m, node_budget=10 ** 9)
+        r = O.exact_pairs(c, m)
+        assert b["proven"] and r["cmax"] == b["cmax"], (trial, n, m)
+
+
 # ------------------------------------------------------------------ N4(a) microbatch order
 def test_order_search_survey_counterexample(O):
     # SURVEY appendix 1: F = [[1,5],[5,1]], B = 2F gives 29 in slot order, 25 reversed
