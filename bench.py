@@ -105,6 +105,25 @@ def int_peaks():
     return json.load(open(f)) if os.path.exists(f) else None
 
 
+def stage_a_ops_per_pair(model, mem):
+    """fp64 arithmetic operations (add/sub/mul/div, one each) of one Stage-A (config, N_mb)
+    pair as csrc/stage_a.cu evaluates Algorithm 1 (O9), for the model's
+    grid shapes: (memory part, everything after the Eq. (4)-(5) check)."""
+    def lerp1d(nx):
+        return 0 if nx == 1 else 7                       # w = (x - x_k) / (x_k+1 - x_k); dlerp
+    def interp_thr(g):
+        l1 = lerp1d(len(g["x"]))
+        return l1 if len(g["tp"]) == 1 else 3 + 2 * l1 + 4
+    def interp_mem(g):
+        l1 = lerp1d(len(g["x"]))
+        plane = l1 if len(g["tp"]) == 1 else 3 + 2 * l1 + 4
+        return 3 + 2 * plane + 4
+    mem_part = 6 + 4 + sum(interp_mem(mem[k]) for k in ("ms_e", "as_e", "ms_l", "as_l"))
+    rest = 13 + (1 if model.get("e_attn") else 0) + 1 + 4 + 2 + 3 + 1 + 7 + 2 + \
+        interp_thr(model["thr_e"]) + interp_thr(model["thr_att"]) + interp_thr(model["thr_lin"])
+    return mem_part, rest
+
+
 # ---------------------------------------------------------------- clocks (NVML)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -417,8 +436,26 @@ def main():
                 "peak_alu_pipe": peak_alu, "frac_alu_pipe": achieved / peak_alu,
                 "kernel_ms": cand_ms, "kernel_share_of_step": cand_ms / ms_per_step,
                 "peak_note": note, "ops_per_candidate": ops_launch / max(1, (e - b) * P)}
+    stage_a = None
     if alg1:
         roofline["kernel"] = "k_candidates<u32> x P plans (Stage B, 4 streams)"
+        # Stage A alone (k_stage_a, fp64 closed forms over every (config, N_mb) pair), timed by
+        # the library's events over the timed steps; roofline against the measured fp64 rate
+        if prof.get("stage_a_launches"):
+            sa_ms = prof["stage_a_ms"] / prof["stage_a_launches"]
+            mem_ops, rest_ops = stage_a_ops_per_pair(p.model, p.mem())
+            ops = res["n_pairs"] * mem_ops + res["n_feasible"] * rest_ops
+            ach = ops / (sa_ms / 1e3) / 1e12
+            stage_a = {"kernel": "k_stage_a", "ms": sa_ms, "pairs": res["n_pairs"], "feasible": res["n_feasible"],
+                       "pairs_per_s": res["n_pairs"] / (sa_ms / 1e3), "share_of_step": sa_ms / ms_per_step,
+                       "fp64_ops_per_pair": {"memory_check": mem_ops, "durations": rest_ops},
+                       "roofline": {"bound": "fp64", "achieved": ach, "unit": "Tops/s"}}
+            if ip and "dadd_f64" in ip:
+                pk = ip["dadd_f64"]["lane_ops_per_s"] / 1e12
+                stage_a["roofline"].update(peak=pk, frac=ach / pk,
+                                           peak_note="measured DADD/DMUL lane-ops/s (profiles/int_peaks.json, 64 per "
+                                                     "clk per SM); a DDIV counts one algorithmic op but issues a "
+                                                     "Newton sequence of ~10 fp64 instructions")
         roofline["duration_note"] = "device step time (Stage A + Stage B)"
     # traffic: dram__bytes_read.sum + dram__bytes_write.sum of the candidate kernel from the
     # committed ncu --set full capture (profiles/traffic.json), per candidate x this launch's K
@@ -452,6 +489,7 @@ def main():
         "winner": {"batch": (args.warmup + args.steps - 1) % n_batches, "cand": res["cand"],
                    "makespan_ticks": res["makespan"], "cmax_ticks": res["cmax"], "plan": res["plan"]},
         "kernel_variant": variant,
+        "stage_a": stage_a,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample, thr = oracle_rate(p, K, args.cpu_seconds)

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DFLOP_ABI_VERSION 3u
+#define DFLOP_ABI_VERSION 4u
 
 typedef int32_t dflop_status;
 #define DFLOP_OK 0
@@ -226,14 +226,17 @@ dflop_status dflop_release_caches(void);
 
 /* ---------------------------------------------------------------- instrumentation
  * A process-wide counter of every kernel the library launches, and (when enabled) CUDA
- * events recorded on the launching stream around each candidate-kernel launch (a3/a4),
- * so that a benchmark can time the dominant kernel live.  dflop_profile_read synchronises
+ * events recorded on the launching stream around each candidate-kernel launch (a3/a4) and
+ * each Stage-A kernel (a6, k_stage_a), so that a benchmark can time them live.  dflop_profile_read synchronises
  * the recorded events, fills *out and, if reset != 0, clears the counters. */
 typedef struct dflop_profile {
     uint32_t struct_size;
     uint32_t cand_launches;   /* candidate-kernel launches timed                      */
     uint64_t kernel_launches; /* all libdflop kernel launches since the last reset    */
     double cand_ms;           /* summed device time of the timed candidate launches   */
+    uint32_t stage_a_launches; /* Stage-A kernel launches timed (ALG1 searches)        */
+    uint32_t reserved;
+    double stage_a_ms;        /* their summed device time                            */
 } dflop_profile;
 dflop_status dflop_profile_enable(int on);
 dflop_status dflop_profile_read(dflop_profile* out, int reset);

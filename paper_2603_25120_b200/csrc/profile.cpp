@@ -18,6 +18,7 @@ struct Mark {
 };
 std::vector<Mark> g_marks;   // recorded, not yet read
 std::vector<Mark> g_free;    // reusable events
+std::vector<Mark> g_stage;   // Stage-A kernel marks (e[0], e[1])
 }  // namespace
 
 void count_launches(uint32_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
@@ -36,6 +37,27 @@ int prof_begin(cudaStream_t s) {
     cudaEventRecord(m.e[0], s);
     g_marks.push_back(m);
     return (int)g_marks.size() - 1;
+}
+
+int prof_stage_begin(cudaStream_t s) {
+    if (!profiling()) return -1;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Mark m;
+    if (!g_free.empty()) {
+        m = g_free.back();
+        g_free.pop_back();
+    } else {
+        for (auto& e : m.e) cudaEventCreate(&e);
+    }
+    cudaEventRecord(m.e[0], s);
+    g_stage.push_back(m);
+    return (int)g_stage.size() - 1;
+}
+
+void prof_stage_end(int idx, cudaStream_t s) {
+    if (idx < 0) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (idx < (int)g_stage.size()) cudaEventRecord(g_stage[idx].e[1], s);
 }
 
 void prof_mark(int idx, int which, cudaStream_t s) {  // which = 1..3
@@ -89,12 +111,25 @@ extern "C" dflop_status dflop_profile_read(dflop_profile* out, int reset) {
         }
         ms += best;
     }
+    double sms = 0.0;
+    for (auto& m : g_stage) {
+        cudaError_t e = cudaEventSynchronize(m.e[1]);
+        if (e != cudaSuccess) return cuda_status(e, "profile event");
+        float t = 0.f;
+        cudaEventElapsedTime(&t, m.e[0], m.e[1]);
+        sms += t;
+    }
     out->cand_launches = (uint32_t)g_marks.size();
     out->kernel_launches = g_launches.load();
     out->cand_ms = ms;
+    out->stage_a_launches = (uint32_t)g_stage.size();
+    out->reserved = 0;
+    out->stage_a_ms = sms;
     if (reset) {
         for (auto& m : g_marks) g_free.push_back(m);
+        for (auto& m : g_stage) g_free.push_back(m);
         g_marks.clear();
+        g_stage.clear();
         g_launches.store(0);
     }
     return DFLOP_OK;

@@ -388,7 +388,9 @@ dflop_status stage_a_launch(const dflop_cost_model* cm, const dflop_mem_model* m
     cudaFuncSetAttribute(reinterpret_cast<const void*>(&k_stage_a), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)dyn);
     StageAArgs a{d_cfgs, d_pair_start, d_sums, reinterpret_cast<u64*>(stage_a_out), bT, bP, d_n_feasible};
+    const int mark = prof_stage_begin(s);
     k_stage_a<<<grid, threads, dyn, s>>>(d_k, a);
+    prof_stage_end(mark, s);
     const size_t dyn2 = (size_t)NP * 12 + 16;
     cudaFuncSetAttribute(reinterpret_cast<const void*>(&k_top_merge), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)dyn2);

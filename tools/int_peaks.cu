@@ -78,6 +78,39 @@ __global__ void k_tput(uint32_t iters, uint32_t seed, uint32_t* out, uint64_t* c
     }
 }
 
+// fp64 chains (Stage A of the plan search runs fp64 closed forms): DFMA / DADD / DMUL
+enum F64Op { DFMA = 0, DADD = 1, DMUL = 2 };
+template <int OP, int ILP>
+__global__ void k_tput_f64(uint32_t iters, uint32_t seed, uint32_t* out, uint64_t* clk, uint64_t* ns) {
+    double a[ILP];
+#pragma unroll
+    for (int k = 0; k < ILP; k++) a[k] = 1.0 + 1e-9 * (threadIdx.x * (k + 1) + seed);
+    __syncthreads();
+    uint64_t c0 = clock64(), t0 = gtimer();
+    for (uint32_t it = 0; it < iters; it++) {
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+#pragma unroll
+            for (int k = 0; k < ILP; k++) {
+                const double x = a[(k + 1) % ILP], y = a[(k + 3) % ILP];
+                if constexpr (OP == DFMA) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(a[k]) : "d"(x), "d"(y));
+                else if constexpr (OP == DADD) asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(a[k]) : "d"(x));
+                else asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(a[k]) : "d"(x));
+            }
+        }
+    }
+    __syncthreads();
+    uint64_t c1 = clock64(), t1 = gtimer();
+    double r = 0;
+#pragma unroll
+    for (int k = 0; k < ILP; k++) r += a[k];
+    if (r == 1234.5) out[blockIdx.x * blockDim.x + threadIdx.x] = 1;
+    if (threadIdx.x == 0) {
+        clk[blockIdx.x] = c1 - c0;
+        ns[blockIdx.x] = t1 - t0;
+    }
+}
+
 struct Res { double lane_ops_per_clk_sm, warp_inst_per_clk_smsp, mhz, tops, ms; };
 
 template <int OP, int ILP>
@@ -126,6 +159,38 @@ static int run_lat(uint32_t iters, uint32_t* out, uint64_t* dclk, uint64_t* dns,
 }
 
 template <int OP>
+static int one_f64(const char* name, int sms, uint32_t* out, uint64_t* dclk, uint64_t* dns) {
+    const int blocks = 2, threads = 1024, grid = sms * blocks;
+    const uint32_t iters = 4000;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    k_tput_f64<OP, 8><<<grid, threads>>>(iters / 8, 7u, out, dclk, dns);
+    CK(cudaEventRecord(e0));
+    k_tput_f64<OP, 8><<<grid, threads>>>(iters, 7u, out, dclk, dns);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    std::vector<uint64_t> hc(grid), hn(grid);
+    CK(cudaMemcpy(hc.data(), dclk, grid * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hn.data(), dns, grid * 8, cudaMemcpyDeviceToHost));
+    double cyc = 0;
+    std::vector<double> mhz(grid);
+    for (int i = 0; i < grid; i++) {
+        cyc = std::max(cyc, (double)hc[i]);
+        mhz[i] = hn[i] ? (double)hc[i] / (double)hn[i] * 1e3 : 0;
+    }
+    std::sort(mhz.begin(), mhz.end());
+    const double per_sm = (double)iters * 8.0 * 8 * threads * blocks;
+    printf("  \"%s\": {\"lane_ops_per_clk_per_sm\": %.2f, \"warp_inst_per_clk_per_smsp\": %.3f, "
+           "\"sm_mhz_in_kernel\": %.0f, \"lane_ops_per_s\": %.4e, \"ms\": %.3f},\n",
+           name, per_sm / cyc, per_sm / cyc / 128.0, mhz[grid / 2], (double)iters * 8.0 * 8 * threads * grid / (ms * 1e-3), ms);
+    return 0;
+}
+
+template <int OP>
 static int one(const char* name, int sms, uint32_t* out, uint64_t* dclk, uint64_t* dns, bool last) {
     Res r;
     double lat = 0;
@@ -154,6 +219,9 @@ int main() {
     CK(cudaMalloc(&dns, (size_t)sms * 2 * 8));
     printf("{\n  \"gpu\": \"%s\", \"sms\": %d, \"cc\": \"%d.%d\",\n", prop.name, sms, prop.major, prop.minor);
     printf("  \"how\": \"tools/int_peaks.cu: 148 SMs x 2 CTAs x 1024 threads, 8 independent chains per thread, inline-PTX bodies; cycles by clock64 per CTA (max over CTAs), clock by clock64/globaltimer; latency = one warp, one dependent chain\",\n");
+    if (one_f64<DFMA>("dfma_f64", sms, out, dclk, dns)) return 1;
+    if (one_f64<DADD>("dadd_f64", sms, out, dclk, dns)) return 1;
+    if (one_f64<DMUL>("dmul_f64", sms, out, dclk, dns)) return 1;
     if (one<IADD>(kNames[IADD], sms, out, dclk, dns, false)) return 1;
     if (one<IMIN>(kNames[IMIN], sms, out, dclk, dns, false)) return 1;
     if (one<IADDMIN>(kNames[IADDMIN], sms, out, dclk, dns, false)) return 1;
