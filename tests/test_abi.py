@@ -52,6 +52,16 @@ def test_validation_without_gpu(D, presets):
     assert code == 1 and b"thr_e" in D.lib().dflop_last_error()
     code = D.lib().dflop_simulate_1f1b(None, None, 1, 0, 4, None, None, None)
     assert code == 2
+    # exact solver: m = n_mb * l_dp computed in 64 bits (65536 * 65536 must not wrap to 0)
+    big = D.plan_struct(dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=1, l_dp=65536, n_mb=65536))
+    need = C.c_size_t(0)
+    code = D.lib().dflop_exact_cmax(None, 0, C.byref(big), C.c_uint64(1), None, None, C.byref(need), None, None, None)
+    assert code == 1 and b"65535" in D.lib().dflop_last_error()
+    wide = D.plan_struct(dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=1, l_dp=2, n_mb=200))
+    code = D.lib().dflop_exact_cmax(None, 0, C.byref(wide), C.c_uint64(1), None, None, C.byref(need), None, None, None)
+    assert code == 1 and b"> 256" in D.lib().dflop_last_error()
+    # the library's caches are released (nothing allocated on a CPU-only host)
+    assert D.lib().dflop_release_caches() == 0
 
 
 PROBE = r"""
