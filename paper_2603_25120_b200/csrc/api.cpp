@@ -130,7 +130,7 @@ struct BalancePlan {
 };
 
 static dflop_status plan_balance(uint32_t n, const dflop_plan* plan, uint32_t mode, uint32_t R, uint32_t G,
-                                 uint32_t n_cand, BalancePlan* out) {
+                                 uint32_t n_cand, BalancePlan* out, bool split_ok = true) {
     const uint64_t m = (uint64_t)plan->n_mb * plan->l_dp;
     const uint64_t S = (uint64_t)plan->e_pp + plan->l_pp;
     if (n > 65535) {
@@ -159,6 +159,7 @@ static dflop_status plan_balance(uint32_t n, const dflop_plan* plan, uint32_t mo
     sh.G = G;
     sh.n_cand = n_cand;
     sh.D = out->prog.D;
+    sh.split_ok = split_ok ? 1u : 0u;
     out->cfg = balance_config(sh, current_device());
     if (!out->cfg.ok) {
         set_error("%s", out->cfg.why.c_str());
@@ -728,8 +729,13 @@ static dflop_status search_impl(const dflop_cluster* cl, const dflop_cost_model*
                 continue;
             }
             BalancePlan bpn;
-            if ((st = plan_balance(nb, &plans[p], bmode, sp->R, sp->G, cend - cb, &bpn)) != DFLOP_OK)
+            if ((st = plan_balance(nb, &plans[p], bmode, sp->R, sp->G, cend - cb, &bpn, !alg1)) != DFLOP_OK)
                 return st;
+            if (bpn.cfg.total > L.bal_bytes && bpn.cfg.split) {
+                // a smaller batch than the bound's: its split chunk may be longer; run it merged
+                if ((st = plan_balance(nb, &plans[p], bmode, sp->R, sp->G, cend - cb, &bpn, false)) != DFLOP_OK)
+                    return st;
+            }
             if (bpn.cfg.total > L.bal_bytes) {
                 set_error("internal: balance workspace %zu > bound %zu", bpn.cfg.total, L.bal_bytes);
                 return DFLOP_ERR_UNSUPPORTED;

@@ -9,6 +9,7 @@
 //   k_simulate      standalone batched 1F1B (dflop_simulate_1f1b)
 //   k_group_*       CSR index groups ("returns a set of index groups")
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 
@@ -485,6 +486,49 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     }
     cfg.n_slots = 0;
     for (int v = 0; v < 3; ++v) cfg.n_slots = std::max(cfg.n_slots, cfg.grid[v] * cfg.cpb[v]);
+    // split pipeline: the packed variant's LPT in k_lpt with lpt_gl =
+    // m / 32 lanes per candidate and ~0.5 KB of shared memory each (bucket keys + a 16-byte
+    // stage), then the candidate kernel from its output; chunks of r LPT rounds, r chosen so
+    // that the candidate kernel's rounds over a chunk are nearly whole
+    const int split_env = env_int("DFLOP_SPLIT", 1);  // 0: never, 2: whenever eligible (tests)
+    if (sh.split_ok && split_env != 0 && !(sh.mode & DFLOP_MODE_EXHAUSTIVE) && m >= 48 &&
+        !wide && cfg.tbl_smem[0] && n > 0) {
+        int lg = (int)std::min<uint32_t>(8, std::max<uint32_t>(2, next_pow2(m / 32 + 1) / 2));
+        const int flg = env_int("DFLOP_LPT_GL", 0);
+        if (flg == 2 || flg == 4 || flg == 8) lg = flg;
+        const uint32_t lpw = 32u / (uint32_t)lg;  // candidates per warp
+        uint32_t lcb = round16(m * 8u) + 16u;
+        while (lcb % 128 != 8u * (uint32_t)lg) lcb += 16;  // probe loads conflict-free (8-byte banks)
+        const uint32_t ltbl = (uint32_t)(((size_t)n * 16 + 127) & ~(size_t)127);
+        uint32_t lcpb = ltbl < smem_max ? (uint32_t)std::min<size_t>((smem_max - ltbl) / lcb, kLptMaxThreads / lg) : 0;
+        lcpb = lcpb / lpw * lpw;
+        const uint32_t wave = nsm * lcpb, res0 = cfg.grid[0] * cfg.cpb[0];
+        if (lcpb >= 4 * lpw && (sh.n_cand >= 2 * wave || split_env == 2) && res0 > 0) {
+            uint32_t best_r = 4;
+            double best_w = 1e9;
+            for (uint32_t r = 3; r <= 8; ++r) {
+                const double rounds = (double)wave * r / res0;
+                const double w = (std::ceil(rounds) - rounds) / std::ceil(rounds);
+                if (w < best_w - 1e-9) {
+                    best_w = w;
+                    best_r = r;
+                }
+            }
+            const int fr = env_int("DFLOP_SPLIT_ROUNDS", 0);
+            if (fr >= 1 && fr <= 64) best_r = (uint32_t)fr;
+            cfg.split = true;
+            cfg.lpt_gl = lg;
+            cfg.lpt_cb = lcb;
+            cfg.lpt_tbl = ltbl;
+            cfg.lpt_cpb = lcpb;
+            cfg.lpt_grid = nsm;
+            cfg.lpt_chunk = std::min<uint32_t>(sh.n_cand, wave * best_r);
+            const int fch = env_int("DFLOP_SPLIT_CHUNK", 0);  // tests: several chunks at small K
+            if (fch > 0) cfg.lpt_chunk = std::min<uint32_t>(sh.n_cand, (uint32_t)fch);
+            cudaFuncSetAttribute(lpt_kernel_ptr(lg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)((size_t)ltbl + (size_t)lcpb * lcb));
+        }
+    }
     if (env_int("DFLOP_DEBUG", 0))
         fprintf(stderr,
                 "[dflop] balance n=%u m=%u S=%u D=%u gl=%d cap=%u apos=%u | packed/u32/u64: tbl=%u/%u/%u "
@@ -492,6 +536,9 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
                 n, m, S, sh.D, gl, cfg.cap, cfg.apos_bytes, cfg.tbl_bytes[0], cfg.tbl_bytes[1], cfg.tbl_bytes[2],
                 cfg.cand_bytes[0], cfg.cand_bytes[1], cfg.cand_bytes[2], cfg.cpb[0], cfg.cpb[1], cfg.cpb[2],
                 cfg.grid[0], cfg.grid[1], cfg.grid[2], cfg.n_slots);
+    if (cfg.split && env_int("DFLOP_DEBUG", 0))
+        fprintf(stderr, "[dflop] split: lpt gl=%d cpb=%u cand=%u tbl=%u chunk=%u\n", cfg.lpt_gl, cfg.lpt_cpb,
+                cfg.lpt_cb, cfg.lpt_tbl, cfg.lpt_chunk);
     size_t o = 0;
     cfg.o_hdr = o;        o += align256(sizeof(BalanceHeader));
     cfg.o_keys = o;       o += align256((size_t)n * 8);
@@ -506,6 +553,10 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     cfg.o_slot_apos = o;  o += align256((size_t)cfg.n_slots * 2 * cfg.apos_bytes);
     cfg.o_slot_csr = o;   o += align256((size_t)cfg.n_slots * 2 * cfg.csr_len);
     cfg.o_grp = o;        o += groups_ws_bytes(n, m);
+    if (cfg.split) {  // k_lpt -> candidate kernel: per chunk entry (+1 for tail groups)
+        cfg.o_lpt_apos = o;  o += align256(((size_t)cfg.lpt_chunk + 1) * cfg.apos_bytes);
+        cfg.o_lpt_el = o;    o += align256(((size_t)cfg.lpt_chunk + 1) * m * 8);
+    }
     cfg.total = o;
     cfg.ok = true;
     return cfg;
@@ -581,6 +632,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
     p.apos_bytes = cfg.apos_bytes;
     p.phase = phase_counters();
     const int mark = prof_begin(s);
+    uint32_t launches = n > 0 ? 8 : 6;
     for (int v = 0; v < 3; ++v) {
         CandParams q = p;
         q.items = v == 2 ? reinterpret_cast<const void*>(it64) : reinterpret_cast<const void*>(it32);
@@ -599,12 +651,40 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
         cudaFuncSetAttribute(cand_kernel_ptr(v, cfg.gl, cfg.tbl_smem[v], p.order4 != 0),
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)L.dyn);
-        cand_launch(L, q, s);
+        if (v == 0 && cfg.split) {
+            // per chunk: k_lpt, then the packed candidate kernel on its output (both return at
+            // once when another variant runs)
+            CandParams ql = q;
+            ql.tbl_bytes = cfg.lpt_tbl;
+            ql.cand_bytes = cfg.lpt_cb;
+            ql.off_scr = round16(a.sh.m * 8u);
+            ql.lpt_apos = reinterpret_cast<uint8_t*>(ws + cfg.o_lpt_apos);
+            ql.lpt_el = reinterpret_cast<uint32_t*>(ws + cfg.o_lpt_el);
+            q.lpt_apos = ql.lpt_apos;
+            q.lpt_el = ql.lpt_el;
+            q.lpt_in = 1;
+            const size_t ldyn = (size_t)cfg.lpt_tbl + (size_t)cfg.lpt_cpb * cfg.lpt_cb;
+            cudaFuncSetAttribute(lpt_kernel_ptr(cfg.lpt_gl), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ldyn);
+            for (uint32_t c0 = a.c_begin; c0 < a.c_end; c0 += cfg.lpt_chunk) {
+                ql.c_begin = q.c_begin = c0;
+                ql.c_end = q.c_end = std::min(a.c_end, c0 + cfg.lpt_chunk);
+                if (p.cand_T) {  // the per-candidate arrays are indexed from a.c_begin
+                    q.cand_T = p.cand_T + (c0 - a.c_begin);
+                    q.cand_cmax = p.cand_cmax + (c0 - a.c_begin);
+                }
+                lpt_launch(cfg.lpt_gl, cfg.lpt_grid, cfg.lpt_cpb, ldyn, ql, s);
+                cand_launch(L, q, s);
+                launches += 2;
+            }
+            launches -= 1;
+        } else {
+            cand_launch(L, q, s);
+        }
         prof_mark(mark, v + 1, s);
     }
     k_finalize<<<1, 256, 0, s>>>(hdr, slot_key, slot_T, slot_cmax, slot_buf, slot_apos, cfg.n_slots, cfg.apos_bytes,
                                  a.sh.m > 255, order, n, a.id_base, a.best, a.assign);
-    count_launches(n > 0 ? 8 : 6);
+    count_launches(launches);
     return cuda_status(cudaGetLastError(), "balance launch");
 }
 

@@ -46,6 +46,14 @@ struct CandParams {
     uint32_t order4;             // DFLOP_MODE_ORDER4: best of four slot orders per replica
     uint32_t tbl_bytes, cand_bytes, off_fl, off_scr;
     unsigned long long* phase;   // diagnostic phase counters (timing builds), else null
+    // split pipeline (packed variant): k_lpt runs the LPT of the candidates [c_begin, c_end)
+    // and leaves, per candidate c, its assignment at lpt_apos + (c - c_begin) * apos_bytes and
+    // its bucket loads (E, L packed keys, m x 2 u32) at lpt_el + (c - c_begin) * 2m; entry
+    // c_end - c_begin is a scratch entry for the tail groups; k_candidates with lpt_in = 1
+    // starts every candidate from there
+    uint8_t* lpt_apos;
+    uint32_t* lpt_el;
+    uint32_t lpt_in;
 };
 
 struct CandLaunch {
@@ -58,5 +66,9 @@ struct CandLaunch {
 
 const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem, bool o4);
 void cand_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+// the split pipeline's LPT kernel (packed u32 variant, item table in shared memory)
+constexpr int kLptMaxThreads = 640;
+const void* lpt_kernel_ptr(int gl);
+void lpt_launch(int gl, uint32_t grid, uint32_t cpb, size_t dyn, const CandParams& p, cudaStream_t s);
 
 }  // namespace dflop

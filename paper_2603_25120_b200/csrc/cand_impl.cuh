@@ -466,7 +466,8 @@ DFLOP_DEV void probe_fixed(const Pair2<uint32_t>* EL, uint32_t gl, uint32_t d, u
 template <int GL, bool FIX8>
 DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* apos, uint32_t pa, uint32_t pb,
                              const Pair2<uint32_t> ia, const Pair2<uint32_t> ib, uint32_t jmask,
-                             uint32_t gl, uint32_t m, bool wide, uint32_t co, uint32_t stage_s, uint32_t start) {
+                             uint32_t gl, uint32_t m, bool wide, uint32_t co, uint32_t stage_s, uint32_t start,
+                             bool staged) {
     // never called for c == 0 (its probes use zero items; the single-sample loop does it)
     const uint32_t da = ia.a - ia.b + co, db = ib.a - ib.b + co;  // probe offsets (lpt_pass)
     uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
@@ -530,13 +531,58 @@ DFLOP_DEV void lpt_pair_step(Pair2<uint32_t>* EL, Pair2<uint32_t>* FL, uint8_t* 
     if (own_a) EL[ja] = Pair2<uint32_t>{ela.a + ia.a, ela.b + ia.b};
     const Pair2<uint32_t> elb = EL[jb];  // after A's update in program order when jb = ja (same lane)
     if (own_b) EL[jb] = Pair2<uint32_t>{elb.a + ib.a, elb.b + ib.b};
-    if constexpr (FIX8) {
+    if (FIX8 || staged) {
         if (own_a) sts_u8(stage_s + (pa - start), ja);
         if (own_b) sts_u8(stage_s + (pb - start), jb);
     } else {
         if (own_a) set_apos(apos, pa, ja, wide);
         if (own_b) set_apos(apos, pb, jb, wide);
     }
+}
+
+// lpt_pair_step for exactly Q buckets per lane (m == Q * GL, one-byte assignment, staged),
+// fully unrolled: B's two smallest by sorted pairs merged four buckets at a time (the split
+// pipeline's k_lpt: Q = 32 for m = 64 at GL = 2)
+template <int GL, int Q>
+DFLOP_DEV void lpt_pair_step_q(Pair2<uint32_t>* EL, uint32_t pa, uint32_t pb, const Pair2<uint32_t> ia,
+                               const Pair2<uint32_t> ib, uint32_t jmask, uint32_t gl, uint32_t co,
+                               uint32_t stage_s, uint32_t start) {
+    static_assert(Q % 4 == 0, "Q buckets per lane, a multiple of 4");
+    const uint32_t da = ia.a - ia.b + co, db = ib.a - ib.b + co;
+    uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+#pragma unroll
+    for (uint32_t k = 0; k < Q; k += 4) {
+        const Pair2<uint32_t> x0 = EL[gl + GL * k], x1 = EL[gl + GL * (k + 1)];
+        const Pair2<uint32_t> x2 = EL[gl + GL * (k + 2)], x3 = EL[gl + GL * (k + 3)];
+        a0 = min(a0, min(max(x0.a + da, x0.b), max(x1.a + da, x1.b)));
+        a1 = min(a1, min(max(x2.a + da, x2.b), max(x3.a + da, x3.b)));
+        const uint32_t v0 = max(x0.a + db, x0.b), v1 = max(x1.a + db, x1.b);
+        const uint32_t v2 = max(x2.a + db, x2.b), v3 = max(x3.a + db, x3.b);
+        const uint32_t lo01 = min(v0, v1), hi01 = max(v0, v1), lo23 = min(v2, v3), hi23 = max(v2, v3);
+        const uint32_t l = min(lo01, lo23), h = min(max(lo01, lo23), min(hi01, hi23));
+        m2 = min(min(max(m1, l), m2), h);
+        m1 = min(m1, l);
+    }
+    uint32_t ba = min(a0, a1);
+#pragma unroll
+    for (int off = GL / 2; off > 0; off >>= 1) {
+        ba = min(ba, __shfl_xor_sync(FULL, ba, off));
+        const uint32_t o1 = __shfl_xor_sync(FULL, m1, off), o2 = __shfl_xor_sync(FULL, m2, off);
+        m2 = min(max(m1, o1), min(m2, o2));
+        m1 = min(m1, o1);
+    }
+    const uint32_t ja = ba & jmask;
+    const bool own_a = ((ba ^ gl) & (GL - 1)) == 0;
+    const Pair2<uint32_t> ela = EL[ja];
+    const uint32_t alt = min(m2, max(ela.a + ia.a + db, ela.b + ia.b));
+    const uint32_t kb = ((m1 & jmask) != ja) ? m1 : alt;
+    const uint32_t jb = kb & jmask;
+    const bool own_b = ((kb ^ gl) & (GL - 1)) == 0;
+    if (own_a) EL[ja] = Pair2<uint32_t>{ela.a + ia.a, ela.b + ia.b};
+    const Pair2<uint32_t> elb = EL[jb];
+    if (own_b) EL[jb] = Pair2<uint32_t>{elb.a + ib.a, elb.b + ib.b};
+    if (own_a) sts_u8(stage_s + (pa - start), ja);
+    if (own_b) sts_u8(stage_s + (pb - start), jb);
 }
 
 // ---------------------------------------------------------------- LPT pass (R12)
@@ -564,9 +610,9 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
     const uint32_t W = nc ? max(1u, min((uint32_t)GL, 128u / ((32u / GL) * nc))) : 1u;
     const uint32_t lane = threadIdx.x & 31u, mycg = lane / GL;
     const uint32_t n_groups = (n + G - 1) / G;
-    // one-byte assignments with m == 8 * GL: the group's decisions are staged in the (idle)
-    // refinement scratch and flushed with one 8/16-byte store per base group (flush_stage)
-    const bool stg = !wide && m == 8 * GL;
+    // one-byte assignments: the group's decisions are staged in the (idle) refinement scratch
+    // and flushed with one 8/16-byte store per base group (flush_stage)
+    const bool stg = !wide;
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(scr);
     // The first m decisions are forced when every one of the m largest items has e > 0 and
     // l > 0 (`forced`, k_candidates): at step t < m buckets 0..t-1 hold one such item each and
@@ -610,7 +656,21 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, true>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
-                                            T.el(pb), jmask, gl, m, false, co, stage_s, start);
+                                            T.el(pb), jmask, gl, m, false, co, stage_s, start, true);
+                }
+            } else if (GL <= 4 && m == 32 * GL && !wide) {
+                for (; t + 1 < ng; t += 2) {
+                    const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
+                    const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
+                    lpt_pair_step_q<GL, 32>(reinterpret_cast<Pair2<uint32_t>*>(EL), pa, pb, T.el(pa), T.el(pb),
+                                            jmask, gl, co, stage_s, start);
+                }
+            } else if (GL <= 4 && m == 16 * GL && !wide) {
+                for (; t + 1 < ng; t += 2) {
+                    const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
+                    const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
+                    lpt_pair_step_q<GL, 16>(reinterpret_cast<Pair2<uint32_t>*>(EL), pa, pb, T.el(pa), T.el(pb),
+                                            jmask, gl, co, stage_s, start);
                 }
             } else {
                 for (; t + 1 < ng; t += 2) {
@@ -618,7 +678,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
                     lpt_pair_step<GL, false>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                              reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
-                                             T.el(pb), jmask, gl, m, wide, co, 0u, start);
+                                             T.el(pb), jmask, gl, m, wide, co, stage_s, start, stg);
                 }
             }
         }
@@ -1149,6 +1209,24 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
                              Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, u64& Tc,
                              u64& cmax, PhaseTimer& ph, bool forced) {
     const uint32_t m = p.m;
+    bool from_lpt = false;
+    if constexpr (PK && sizeof(A) == 4) from_lpt = p.lpt_in != 0;
+    if (from_lpt) {
+        // split pipeline: k_lpt left this candidate's packed bucket keys (offset removed) and
+        // its assignment; the caller copied the assignment into apos
+        const uint2* src = reinterpret_cast<const uint2*>(p.lpt_el) + (size_t)(c - p.c_begin) * m;
+        for (uint32_t j = gl; j < m; j += GL) {
+            const uint2 v = __ldcg(src + j);
+            EL[j] = Pair2<A>{(A)v.x, (A)v.y};
+            FL[j] = Pair2<A>{0, 0};
+        }
+        __syncwarp(FULL);
+        ph.mark(0);
+        if (m >= 2 && p.R > 0)
+            refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
+        else
+            form_fl<A, GL, SM>(p, T, apos, p.wide != 0, FL, gl);
+    } else {
     for (uint32_t j = gl; j < m; j += GL) {
         // co: the LPT probe offset; the plain variant's lane-local LPT keys carry k = j / GL
         EL[j] = PK ? Pair2<A>{(A)j, (A)(j + co)}
@@ -1188,6 +1266,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
             refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
         else
             form_fl<A, GL, SM>(p, T, apos, p.wide != 0, FL, gl);
+    }
     }
     A cm = 0;
     for (uint32_t j = gl; j < m; j += GL) {
@@ -1268,8 +1347,16 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         bufs[p.apos_bytes + b] = 0xFF;
     }
     __syncwarp(FULL);
-    uint32_t cur = 0, best_buf = 0;
-    u64 best_key = ~0ull, best_T = 0, best_cmax = 0;
+    // the slot's best so far (k_init sets the keys to ~0): a launch continues the previous
+    // launches' slots (the split pipeline runs the family in chunks)
+    u64 best_key = p.slot_key[slot], best_T = 0, best_cmax = 0;
+    uint32_t best_buf = 0;
+    if (best_key != ~0ull) {
+        best_T = p.slot_T[slot];
+        best_cmax = p.slot_cmax[slot];
+        best_buf = p.slot_buf[slot];
+    }
+    uint32_t cur = best_buf ^ 1u;
     PhaseTimer ph;
     ph.start(p.phase);
     // a full round hands candidates base + block * cpb + grp to the block's groups; a partial
@@ -1282,6 +1369,12 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         if (!__any_sync(FULL, valid)) break;  // warp-uniform: every group of the warp is done
         const uint32_t c = valid ? cc : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
+        if (PK && sizeof(A) == 4 && p.lpt_in) {  // the chunk's assignment from k_lpt into the slot's working buffer
+            const uint4* src = reinterpret_cast<const uint4*>(p.lpt_apos + (size_t)(c - p.c_begin) * p.apos_bytes);
+            uint4* dst = reinterpret_cast<uint4*>(apos);
+            for (uint32_t b = gl; b < p.apos_bytes / 16; b += GL) dst[b] = __ldcg(src + b);
+            __syncwarp(FULL);
+        }
         u64 Tc, cmax;
         run_candidate<A, PK, GL, SM, O4>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph, forced);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
@@ -1313,6 +1406,65 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         p.slot_cmax[slot] = best_cmax;
         p.slot_buf[slot] = best_buf;
         if (best_key != ~0ull) atomicMin(&p.hdr->best_key, best_key);
+    }
+}
+
+// ---------------------------------------------------------------- split pipeline: the LPT alone
+// The LPT pass of the packed variant for the candidates [c_begin, c_end) with few lanes per
+// candidate (GL = m / 32: 32 buckets per lane for m = 64) and only the bucket keys and a
+// 16-byte stage in shared memory per candidate (≈0.5 KB instead of ≈2 KB), so ~300
+// candidates are resident per SM: the per-sample reduction and the two-sample bookkeeping
+// are shared by 4x more buckets per lane.  Writes each candidate's
+// assignment and final packed keys (offset removed) for k_candidates (lpt_in).
+template <int GL>
+__global__ void __launch_bounds__(kLptMaxThreads) k_lpt(CandParams p) {
+    if (p.hdr->variant != 0) return;  // the packed variant only
+    const uint32_t sh = p.hdr->shift, co = p.hdr->offs;
+    extern __shared__ __align__(128) uint8_t smem[];
+    Tbl<uint32_t, true> T;
+    {
+        const uint32_t words = p.n * (uint32_t)sizeof(ItemRec<uint32_t>) / 16;
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
+            reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.items) + i);
+        __syncthreads();
+        T.it = reinterpret_cast<const ItemRec<uint32_t>*>(smem);
+        T.it_s = (uint32_t)__cvta_generic_to_shared(smem);
+        T.pi16 = nullptr;
+        T.pi32 = nullptr;
+    }
+    bool forced = false;  // as in k_candidates
+    if (p.m >= 1 && p.m <= p.n) {
+        bool ok = true;
+        for (uint32_t q = threadIdx.x & 31u; q < p.m; q += 32) {
+            const Pair2<uint32_t> r = T.el(q);
+            ok = ok && r.a != 0 && r.b != 0;
+        }
+        forced = __all_sync(FULL, ok);
+    }
+    const uint32_t grp = threadIdx.x / GL, gl = threadIdx.x % GL;
+    const uint32_t cpb = blockDim.x / GL, m = p.m;
+    uint8_t* base = smem + p.tbl_bytes + (size_t)grp * p.cand_bytes;
+    Pair2<uint32_t>* EL = reinterpret_cast<Pair2<uint32_t>*>(base);
+    uint8_t* stage = base + p.off_scr;
+    const uint32_t span = p.c_end - p.c_begin;
+    const uint32_t stride = gridDim.x * cpb;
+    for (uint32_t b0 = p.c_begin; b0 < p.c_end; b0 += stride) {
+        const uint32_t cc = b0 + (p.c_end - b0 >= stride ? blockIdx.x * cpb + grp : grp * gridDim.x + blockIdx.x);
+        const bool valid = cc < p.c_end;
+        if (!__any_sync(FULL, valid)) break;  // warp-uniform
+        const uint32_t c = valid ? cc : p.c_end - 1;          // tail groups recompute a real candidate
+        const uint32_t e = valid ? cc - p.c_begin : span;     // ... into the scratch entry
+        uint8_t* apos = p.lpt_apos + (size_t)e * p.apos_bytes;
+        for (uint32_t j = gl; j < m; j += GL) EL[j] = Pair2<uint32_t>{j, j + co};
+        for (uint32_t b = p.n + gl; b < p.apos_bytes; b += GL) apos[b] = 0xFF;  // padding: never a bucket
+        __syncwarp(FULL);
+        lpt_pass<uint32_t, true, GL, true>(p, T, c, sh, EL, EL, apos, stage, gl, co, forced);
+        Pair2<uint32_t>* dst = reinterpret_cast<Pair2<uint32_t>*>(p.lpt_el) + (size_t)e * m;
+        for (uint32_t j = gl; j < m; j += GL) {
+            const Pair2<uint32_t> x = EL[j];
+            __stcg(reinterpret_cast<unsigned long long*>(dst + j), pack64(x.b - co, x.a));
+        }
+        __syncwarp(FULL);
     }
 }
 

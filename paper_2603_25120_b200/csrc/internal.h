@@ -70,6 +70,7 @@ struct BalanceShape {
     uint32_t mode, R, G;
     uint32_t n_cand;  // cand_end - cand_begin
     uint32_t D;       // 1F1B ring depth of the slot program
+    uint32_t split_ok = 0;  // the split pipeline may be used (fixed-plan calls)
 };
 struct BalanceConfig {
     int gl = 1;                        // lanes per candidate
@@ -86,9 +87,14 @@ struct BalanceConfig {
     uint32_t cpb[3] = {0, 0, 0};               // candidates per block
     uint32_t grid[3] = {0, 0, 0};
     uint32_t n_slots = 0;
+    // split pipeline (packed variant only): k_lpt with lpt_gl lanes per candidate, then the
+    // candidate kernel on its output, over chunks of lpt_chunk candidates
+    bool split = false;
+    int lpt_gl = 0;
+    uint32_t lpt_cpb = 0, lpt_grid = 0, lpt_tbl = 0, lpt_cb = 0, lpt_chunk = 0;
     // workspace layout (byte offsets)
     size_t o_hdr, o_keys, o_order, o_item_pos, o_items32, o_items64, o_slot_key, o_slot_T, o_slot_cmax,
-        o_slot_buf, o_slot_apos, o_slot_csr, o_grp, total;
+        o_slot_buf, o_slot_apos, o_slot_csr, o_grp, o_lpt_apos = 0, o_lpt_el = 0, total;
     bool ok = false;
     std::string why;
 };

@@ -183,6 +183,40 @@ def test_balance_shard_window_config5(D, O, presets):
     check_balance(D, O, q, p.plan, p.K, p.R, p.G, p.seed(2), 777_000, 777_024)
 
 
+@pytest.mark.parametrize("n, n_mb, l_dp, hi", [
+    (4096, 64, 1, None),      # config 5's shape: k_lpt at GL = 2, 32 buckets per lane
+    (2000, 50, 2, 2 ** 20),   # m = 100: GL = 2, generic bucket loop
+    (1500, 64, 2, 2 ** 18),   # m = 128: GL = 4, 32 buckets per lane
+    (2500, 250, 1, 5000),     # m = 250: GL = 4, generic
+    (40, 64, 1, 2 ** 20),     # n < m
+])
+def test_split_pipeline_parity(D, O, presets, monkeypatch, n, n_mb, l_dp, hi):
+    """The split pipeline (k_lpt, then the candidate kernel from its output)
+    forced on (DFLOP_SPLIT=2) over several chunks: every candidate equals the merged kernel's
+    (DFLOP_SPLIT=0) and, on a window, the oracle's."""
+    p = presets[5]
+    if hi is None:
+        q = O.predict(p.model, p.plan, *p.features(1))[1]
+        plan = p.plan
+    else:
+        rng = np.random.default_rng(n + n_mb)
+        q = rng.integers(0, hi, (4, n), dtype=np.uint64).astype(np.uint32)
+        q[:, rng.random(n) < 0.2] = q[:, [0]]  # exact ties
+        plan = dict(e_tp=1, e_pp=2, e_dp=1, l_tp=1, l_pp=6, l_dp=l_dp, n_mb=n_mb)
+    K, seed = 5000, (3, 4)
+    qd = dev_u32(q)
+    monkeypatch.setenv("DFLOP_SPLIT", "0")
+    merged = gpu_balance(D, qd, plan, K, p.R, p.G, seed, 0, K)
+    monkeypatch.setenv("DFLOP_SPLIT", "2")
+    monkeypatch.setenv("DFLOP_SPLIT_CHUNK", "1700")
+    split = gpu_balance(D, qd, plan, K, p.R, p.G, seed, 0, K)
+    assert (split["cT"] == merged["cT"]).all(), np.nonzero(split["cT"] != merged["cT"])[0][:10]
+    assert (split["cC"] == merged["cC"]).all()
+    assert split["best"] == merged["best"] and (split["assign"] == merged["assign"]).all()
+    monkeypatch.setenv("DFLOP_SPLIT_CHUNK", "10")
+    check_balance(D, O, q, plan, K, p.R, p.G, seed, 1690, 1714)  # across chunk boundaries
+
+
 @pytest.mark.parametrize("case", [
     dict(n=0, plan=dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=2, l_dp=1, n_mb=3)),
     dict(n=1, plan=dict(e_tp=1, e_pp=1, e_dp=1, l_tp=1, l_pp=1, l_dp=1, n_mb=1)),
