@@ -411,6 +411,27 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     const uint32_t nsm = (uint32_t)prop.sms;
     const uint32_t per_warp = 32u / (uint32_t)gl;  // candidate groups per warp
     const int forced_cpb = env_int("DFLOP_MAXCPB", 0);  // occupancy experiments
+    // split pipeline: the packed variant's LPT in k_lpt with lg = m / 32
+    // lanes per candidate and ~0.5 KB of shared memory each (bucket keys + a 16-byte stage),
+    // then the candidate kernel (refinement + 1F1B) from its output, chunk by chunk
+    const int split_env = env_int("DFLOP_SPLIT", 1);  // 0: never, 2: whenever eligible (tests)
+    int lg = (int)std::min<uint32_t>(8, std::max<uint32_t>(2, next_pow2(m / 32 + 1) / 2));
+    const int flg = env_int("DFLOP_LPT_GL", 0);
+    if (flg == 1 || flg == 2 || flg == 4 || flg == 8) lg = flg;
+    const uint32_t lpw = 32u / (uint32_t)lg;  // candidates per warp
+    uint32_t lcb = round16(m * 8u) + 16u;
+    if (lg == 1)  // 8-byte loads of 16 lanes (candidates) on distinct bank pairs: stride/8 odd
+        lcb += 8;
+    else
+        while (lcb % 128 != 8u * (uint32_t)lg) lcb += 16;  // probe loads conflict-free (8-byte banks)
+    const uint32_t ltbl = (uint32_t)(((size_t)n * 16 + 127) & ~(size_t)127);
+    uint32_t lcpb = ltbl < smem_max ? (uint32_t)std::min<size_t>((smem_max - ltbl) / lcb, kLptMaxThreads / lg) : 0;
+    lcpb = lcpb / lpw * lpw;
+    const bool split_pre = sh.split_ok && split_env != 0 && !(sh.mode & DFLOP_MODE_EXHAUSTIVE) && m >= 48 &&
+                           !wide && n > 0 && lcpb >= 4 * lpw && (sh.n_cand >= 2 * nsm * lcpb || split_env == 2);
+    // the split candidate kernel runs no LPT: stagger its candidates for the refinement's
+    // broadcast reads (4 candidates of a warp on distinct banks) instead of the probe loads
+    const int stg_env = env_int("DFLOP_SPLIT_STAGGER", 48);
     struct Lay {
         uint32_t cb, tbl, cpb;
         bool tbl_smem;
@@ -422,7 +443,8 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         const uint32_t el = round16(m * 2u * asz);   // EL[m] then FL[m]
         uint32_t cb = 2 * el + scr;
         // stagger consecutive candidates across banks: a group's probe touches GL*2*asz bytes
-        const uint32_t span = std::max(16u, (uint32_t)gl * 2u * asz);
+        uint32_t span = std::max(16u, (uint32_t)gl * 2u * asz);
+        if (v == 0 && split_pre && stg_env >= 16 && stg_env < 128 && stg_env % 16 == 0) span = (uint32_t)stg_env;
         if (span < 128) {
             const uint32_t want = span;  // a multiple of 16 below 128: reachable in <= 7 steps
             while (cb % 128 != want) cb += 16;
@@ -486,48 +508,33 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     }
     cfg.n_slots = 0;
     for (int v = 0; v < 3; ++v) cfg.n_slots = std::max(cfg.n_slots, cfg.grid[v] * cfg.cpb[v]);
-    // split pipeline: the packed variant's LPT in k_lpt with lpt_gl =
-    // m / 32 lanes per candidate and ~0.5 KB of shared memory each (bucket keys + a 16-byte
-    // stage), then the candidate kernel from its output; chunks of r LPT rounds, r chosen so
-    // that the candidate kernel's rounds over a chunk are nearly whole
-    const int split_env = env_int("DFLOP_SPLIT", 1);  // 0: never, 2: whenever eligible (tests)
-    if (sh.split_ok && split_env != 0 && !(sh.mode & DFLOP_MODE_EXHAUSTIVE) && m >= 48 &&
-        !wide && cfg.tbl_smem[0] && n > 0) {
-        int lg = (int)std::min<uint32_t>(8, std::max<uint32_t>(2, next_pow2(m / 32 + 1) / 2));
-        const int flg = env_int("DFLOP_LPT_GL", 0);
-        if (flg == 2 || flg == 4 || flg == 8) lg = flg;
-        const uint32_t lpw = 32u / (uint32_t)lg;  // candidates per warp
-        uint32_t lcb = round16(m * 8u) + 16u;
-        while (lcb % 128 != 8u * (uint32_t)lg) lcb += 16;  // probe loads conflict-free (8-byte banks)
-        const uint32_t ltbl = (uint32_t)(((size_t)n * 16 + 127) & ~(size_t)127);
-        uint32_t lcpb = ltbl < smem_max ? (uint32_t)std::min<size_t>((smem_max - ltbl) / lcb, kLptMaxThreads / lg) : 0;
-        lcpb = lcpb / lpw * lpw;
+    if (split_pre && cfg.tbl_smem[0] && cfg.cpb[0] > 0) {
+        // chunks of r LPT rounds, r chosen so that the candidate kernel's rounds over a chunk
+        // are nearly whole
         const uint32_t wave = nsm * lcpb, res0 = cfg.grid[0] * cfg.cpb[0];
-        if (lcpb >= 4 * lpw && (sh.n_cand >= 2 * wave || split_env == 2) && res0 > 0) {
-            uint32_t best_r = 4;
-            double best_w = 1e9;
-            for (uint32_t r = 3; r <= 8; ++r) {
-                const double rounds = (double)wave * r / res0;
-                const double w = (std::ceil(rounds) - rounds) / std::ceil(rounds);
-                if (w < best_w - 1e-9) {
-                    best_w = w;
-                    best_r = r;
-                }
+        uint32_t best_r = 4;
+        double best_w = 1e9;
+        for (uint32_t r = 3; r <= 8; ++r) {
+            const double rounds = (double)wave * r / res0;
+            const double w = (std::ceil(rounds) - rounds) / std::ceil(rounds);
+            if (w < best_w - 1e-9) {
+                best_w = w;
+                best_r = r;
             }
-            const int fr = env_int("DFLOP_SPLIT_ROUNDS", 0);
-            if (fr >= 1 && fr <= 64) best_r = (uint32_t)fr;
-            cfg.split = true;
-            cfg.lpt_gl = lg;
-            cfg.lpt_cb = lcb;
-            cfg.lpt_tbl = ltbl;
-            cfg.lpt_cpb = lcpb;
-            cfg.lpt_grid = nsm;
-            cfg.lpt_chunk = std::min<uint32_t>(sh.n_cand, wave * best_r);
-            const int fch = env_int("DFLOP_SPLIT_CHUNK", 0);  // tests: several chunks at small K
-            if (fch > 0) cfg.lpt_chunk = std::min<uint32_t>(sh.n_cand, (uint32_t)fch);
-            cudaFuncSetAttribute(lpt_kernel_ptr(lg), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)((size_t)ltbl + (size_t)lcpb * lcb));
         }
+        const int fr = env_int("DFLOP_SPLIT_ROUNDS", 0);
+        if (fr >= 1 && fr <= 64) best_r = (uint32_t)fr;
+        cfg.split = true;
+        cfg.lpt_gl = lg;
+        cfg.lpt_cb = lcb;
+        cfg.lpt_tbl = ltbl;
+        cfg.lpt_cpb = lcpb;
+        cfg.lpt_grid = nsm;
+        cfg.lpt_chunk = std::min<uint32_t>(sh.n_cand, wave * best_r);
+        const int fch = env_int("DFLOP_SPLIT_CHUNK", 0);  // tests: several chunks at small K
+        if (fch > 0) cfg.lpt_chunk = std::min<uint32_t>(sh.n_cand, (uint32_t)fch);
+        cudaFuncSetAttribute(lpt_kernel_ptr(lg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((size_t)ltbl + (size_t)lcpb * lcb));
     }
     if (env_int("DFLOP_DEBUG", 0))
         fprintf(stderr,

@@ -307,7 +307,14 @@ DFLOP_DEV void flush_stage(uint8_t* apos, uint32_t stage_s, uint32_t start, uint
     if (ng == 8 && (start & 7u) == 0) {
         if (gl == 0) *reinterpret_cast<uint2*>(apos + start) = lds_v2(stage_s);
     } else if (ng == 16 && (start & 15u) == 0) {
-        if (gl == 0) *reinterpret_cast<uint4*>(apos + start) = lds_v4(stage_s);
+        if (gl == 0) {
+            if ((stage_s & 15u) == 0) {
+                *reinterpret_cast<uint4*>(apos + start) = lds_v4(stage_s);
+            } else {  // an 8-byte aligned stage (k_lpt with one lane per candidate)
+                const uint2 lo = lds_v2(stage_s), hi = lds_v2(stage_s + 8);
+                *reinterpret_cast<uint4*>(apos + start) = make_uint4(lo.x, lo.y, hi.x, hi.y);
+            }
+        }
     } else {
         for (uint32_t u = gl; u < ng; u += GL) apos[start + u] = (uint8_t)lds_u8(stage_s + u);
     }
@@ -657,6 +664,13 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
                     lpt_pair_step<GL, true>(reinterpret_cast<Pair2<uint32_t>*>(EL),
                                             reinterpret_cast<Pair2<uint32_t>*>(FL), apos, pa, pb, T.el(pa),
                                             T.el(pb), jmask, gl, m, false, co, stage_s, start, true);
+                }
+            } else if (GL == 1 && m == 64 && !wide) {
+                for (; t + 1 < ng; t += 2) {
+                    const uint32_t pa = start + (uint32_t)((perm >> (4 * t)) & 15ull);
+                    const uint32_t pb = start + (uint32_t)((perm >> (4 * (t + 1))) & 15ull);
+                    lpt_pair_step_q<GL, 64>(reinterpret_cast<Pair2<uint32_t>*>(EL), pa, pb, T.el(pa), T.el(pb),
+                                            jmask, gl, co, stage_s, start);
                 }
             } else if (GL <= 4 && m == 32 * GL && !wide) {
                 for (; t + 1 < ng; t += 2) {
