@@ -431,7 +431,8 @@ def main():
         peak_alu = peak_issue / 2
         note = "fallback: 148 SM x 4 SMSP x 32 lanes x 1965 MHz (profiles/int_peaks.json missing)"
     variant = "u64" if wide_sums else "u32"
-    roofline = {"bound": "issue", "kernel": f"k_candidates<{variant}>", "achieved": achieved, "peak": peak_issue,
+    kname = f"k_candidates<{variant}>" if variant == "u64" else "k_lpt + k_candidates<u32> (split pipeline)"
+    roofline = {"bound": "issue", "kernel": kname, "achieved": achieved, "peak": peak_issue,
                 "unit": "Tops/s", "frac": achieved / peak_issue, "traffic": None,
                 "peak_alu_pipe": peak_alu, "frac_alu_pipe": achieved / peak_alu,
                 "kernel_ms": cand_ms, "kernel_share_of_step": cand_ms / ms_per_step,

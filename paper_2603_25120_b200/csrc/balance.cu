@@ -428,7 +428,8 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     uint32_t lcpb = ltbl < smem_max ? (uint32_t)std::min<size_t>((smem_max - ltbl) / lcb, kLptMaxThreads / lg) : 0;
     lcpb = lcpb / lpw * lpw;
     const bool split_pre = sh.split_ok && split_env != 0 && !(sh.mode & DFLOP_MODE_EXHAUSTIVE) && m >= 48 &&
-                           !wide && n > 0 && lcpb >= 4 * lpw && (sh.n_cand >= 2 * nsm * lcpb || split_env == 2);
+                           !wide && n > 0 && gl >= 8 && lcpb >= 4 * lpw &&
+                           (sh.n_cand >= 2 * nsm * lcpb || split_env == 2);
     // the split candidate kernel runs no LPT: stagger its candidates for the refinement's
     // broadcast reads (4 candidates of a warp on distinct banks) instead of the probe loads
     const int stg_env = env_int("DFLOP_SPLIT_STAGGER", 48);
@@ -436,12 +437,16 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         uint32_t cb, tbl, cpb;
         bool tbl_smem;
     };
+    // gather mode of the split candidate kernel (CandParams::gather): FL shares the scratch
+    bool gat = split_pre && env_int("DFLOP_SPLIT_GATHER", 0) != 0;
     auto layout = [&](int v, uint32_t cap) {
         Lay L;
         const uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cap, rings));
         const uint32_t asz = v == 2 ? 8u : 4u;
         const uint32_t el = round16(m * 2u * asz);   // EL[m] then FL[m]
         uint32_t cb = 2 * el + scr;
+        if (v == 0 && gat)  // EL, then {cnt, off, ls, lp8} during the refinement / {rings, FL} after
+            cb = el + std::max(round16(4u * (2u * m + 1u) + 2u * cap) + 8u * cap, round16(rings) + el);
         // stagger consecutive candidates across banks: a group's probe touches GL*2*asz bytes
         uint32_t span = std::max(16u, (uint32_t)gl * 2u * asz);
         if (v == 0 && split_pre && stg_env >= 16 && stg_env < 128 && stg_env % 16 == 0) span = (uint32_t)stg_env;
@@ -453,6 +458,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         const uint32_t tbl = (uint32_t)(((size_t)n * (v == 2 ? 32u : 16u) + (size_t)n * 2 + 127) & ~(size_t)127);
         // stage the table in shared memory when it leaves room for at least 2 warps of candidates
         L.tbl_smem = (size_t)tbl + (size_t)2 * per_warp * cb <= smem_max;
+        if (v == 0 && split_pre && env_int("DFLOP_SPLIT_GTBL", 0)) L.tbl_smem = false;
         L.tbl = L.tbl_smem ? tbl : 0;
         uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - L.tbl) / cb, kCandMaxThreads / gl);
         // no more groups than the family needs (one CTA per SM), whole warps only
@@ -467,6 +473,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     // length, shrunk (not below 32) while that buys resident candidates -- occupancy hides the
     // latency of the shared-memory and shuffle chains (config 5: cap 128 -> 104 raises 72 -> 80
     // candidates per SM, -6.7%; 768-thread blocks would need <= 80 registers: +37%)
+    for (int attempt = 0; attempt < 2; ++attempt) {
     uint32_t cap = std::min(128u, std::max(32u, next_pow2(2 * std::max(1u, per_bucket))));
     {
         uint32_t best = cap, best_cpb = layout(0, cap).cpb;
@@ -490,6 +497,10 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         cfg.tbl_bytes[v] = L.tbl;
         cfg.off_fl[v] = round16(m * 2u * (v == 2 ? 8u : 4u));
         cfg.off_scr[v] = 2 * cfg.off_fl[v];
+        if (v == 0 && gat) {
+            cfg.off_scr[v] = cfg.off_fl[v];
+            cfg.off_fl[v] = cfg.off_scr[v] + round16(rings);
+        }
         if (cpb == 0) {
             char buf[200];
             snprintf(buf, sizeof buf,
@@ -506,9 +517,17 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         cfg.cpb[v] = cpb;
         cfg.grid[v] = std::max(1u, std::min<uint32_t>(want, nsm));
     }
+    // the gather layout only with the split pipeline (the merged kernel maintains FL)
+    if (gat && !(cfg.tbl_smem[0] || env_int("DFLOP_SPLIT_GTBL", 0))) {
+        gat = false;
+        continue;
+    }
+    break;
+    }
+    cfg.gather = gat;
     cfg.n_slots = 0;
     for (int v = 0; v < 3; ++v) cfg.n_slots = std::max(cfg.n_slots, cfg.grid[v] * cfg.cpb[v]);
-    if (split_pre && cfg.tbl_smem[0] && cfg.cpb[0] > 0) {
+    if (split_pre && (cfg.tbl_smem[0] || env_int("DFLOP_SPLIT_GTBL", 0)) && cfg.cpb[0] > 0) {
         // chunks of r LPT rounds, r chosen so that the candidate kernel's rounds over a chunk
         // are nearly whole
         const uint32_t wave = nsm * lcpb, res0 = cfg.grid[0] * cfg.cpb[0];
@@ -535,6 +554,9 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         if (fch > 0) cfg.lpt_chunk = std::min<uint32_t>(sh.n_cand, (uint32_t)fch);
         cudaFuncSetAttribute(lpt_kernel_ptr(lg), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)((size_t)ltbl + (size_t)lcpb * lcb));
+        cudaFuncSetAttribute(split_kernel_ptr(cfg.gather ? 2 : 1, gl, (sh.mode & DFLOP_MODE_ORDER4) != 0),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((size_t)cfg.tbl_bytes[0] + (size_t)cfg.cpb[0] * cfg.cand_bytes[0]));
     }
     if (env_int("DFLOP_DEBUG", 0))
         fprintf(stderr,
@@ -670,7 +692,10 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
             q.lpt_apos = ql.lpt_apos;
             q.lpt_el = ql.lpt_el;
             q.lpt_in = 1;
+            q.gather = cfg.gather ? 1u : 0u;
             const size_t ldyn = (size_t)cfg.lpt_tbl + (size_t)cfg.lpt_cpb * cfg.lpt_cb;
+            cudaFuncSetAttribute(split_kernel_ptr(cfg.gather ? 2 : 1, cfg.gl, p.order4 != 0),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.dyn);
             cudaFuncSetAttribute(lpt_kernel_ptr(cfg.lpt_gl), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ldyn);
             for (uint32_t c0 = a.c_begin; c0 < a.c_end; c0 += cfg.lpt_chunk) {
                 ql.c_begin = q.c_begin = c0;
@@ -680,7 +705,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
                     q.cand_cmax = p.cand_cmax + (c0 - a.c_begin);
                 }
                 lpt_launch(cfg.lpt_gl, cfg.lpt_grid, cfg.lpt_cpb, ldyn, ql, s);
-                cand_launch(L, q, s);
+                split_launch(cfg.gather ? 2 : 1, L, q, s);
                 launches += 2;
             }
             launches -= 1;

@@ -54,6 +54,11 @@ struct CandParams {
     uint8_t* lpt_apos;
     uint32_t* lpt_el;
     uint32_t lpt_in;
+    // gather mode (split pipeline, 32-bit sums, m <= 256): each refinement round copies the
+    // (e, l) records of j''s first cap members into the scratch (lp8, 8 B each) so the pair
+    // search reads partners without table lookups; FL is not maintained during refinement but
+    // formed from the final assignment, in the scratch after the 1F1B rings (off_fl)
+    uint32_t gather;
 };
 
 struct CandLaunch {
@@ -66,6 +71,10 @@ struct CandLaunch {
 
 const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem, bool o4);
 void cand_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+// the split pipeline's candidate kernel (packed u32, shared-memory table, GL in {8, 16, 32});
+// mode 1: from k_lpt's output, mode 2: the same in gather mode (CandParams::gather)
+const void* split_kernel_ptr(int mode, int gl, bool o4);
+void split_launch(int mode, const CandLaunch& L, const CandParams& p, cudaStream_t s);
 // the split pipeline's LPT kernel (packed u32 variant, item table in shared memory)
 constexpr int kLptMaxThreads = 640;
 const void* lpt_kernel_ptr(int gl);

@@ -803,7 +803,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
 // ---------------------------------------------------------------- swap refinement (O6)
 // `apply` is false for c < 2: the rounds are still executed (and discarded) so that every
 // group of a warp issues the same shuffle sequence.
-template <typename A, bool PK, int GL, bool SM>
+template <typename A, bool PK, int GL, bool SM, bool GA = false>
 DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
                       uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, bool apply, PhaseTimer& ph) {
     const uint32_t m = p.m, cap = p.cap;
@@ -823,8 +823,11 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
     }
     uint32_t* off = cnt + m;
     uint16_t* lp = ls + cap;
+    // gather mode (CandParams::gather): j''s records instead of its positions, 16-byte aligned
+    constexpr bool gath = GA && sizeof(A) == 4;
+    Pair2<A>* lp8 = reinterpret_cast<Pair2<A>*>(scr + ((4u * (2u * m + 1u) + 2u * cap + 15u) & ~15u));
     bool dirty = true;  // the lists must be (re)built from the assignment
-    bool first = true;  // the first build also forms FL (LPT maintains EL only)
+    bool first = !gath;  // the first build also forms FL (LPT maintains EL only)
     for (uint32_t r = 0; r < p.R; ++r) {
         if (__any_sync(FULL, dirty)) {  // warp-uniform: a clean group rebuilds the same lists
             build_lists<A, GL, SM>(p, T, apos, wide, cnt, off, csr, gl, first ? FL : nullptr);
@@ -874,14 +877,16 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         {
             const uint32_t na = min(nA, cap), nb = min(nB, cap);
             for (uint32_t u = gl; u < na; u += GL) ls[u] = __ldcg(gss + u);
-            for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + u);
+            if (gath)
+                for (uint32_t u = gl; u < nb; u += GL) lp8[u] = T.el(__ldcg(gsp + u));
+            else
+                for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + u);
         }
         __syncwarp(FULL);
         ph.mark(2);
         A bsc = amax<A>();
-        uint32_t bi = 0xFFFFFFFFu, brk = 0xFFFFFFFFu;
+        uint32_t bi = 0xFFFFFFFFu, brk = 0xFFFFFFFFu, vstar = 0xFFFFFFFFu;
         u64 bkey = ~0ull;  // 32-bit scores: (row minimum << 32 | item), branch-free minima
-        const uint32_t nBs = min(nB, cap);
         // all (i, i') with i in j*, i' in {NONE} u j'; lexicographic min of (score, i, rank(i'))
         // two j* members per lane and step: every j' member loaded once serves two pairs
         auto ival = [&](uint32_t u, uint32_t& ii, A& se, A& sl, A& pe, A& pl) {
@@ -893,7 +898,13 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             pe = Bp.a + a.a;  // j' with i
             pl = Bp.b + a.b;
         };
-        for (uint32_t u = gl; u < nA; u += 2 * GL) {
+        // j''s members in chunks of cap: each chunk copied to shared memory (the first above)
+        // and paired with every row; the row minima fold into bkey chunk by chunk (the NONE
+        // pair in every chunk: idempotent)
+        const bool one_chunk = nB <= cap;  // phase 2 / apply may read the copy
+        for (uint32_t p0 = 0;;) {
+        const uint32_t nBs = p0 < nB ? min(cap, nB - p0) : 0u;
+        for (uint32_t u = gl; u < nA && (p0 == 0 || nBs > 0); u += 2 * GL) {
             uint32_t i0, i1;
             A se0, sl0, pe0, pl0, se1, sl1, pe1, pl1;
             ival(u, i0, se0, sl0, pe0, pl0);
@@ -914,6 +925,12 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 lex_update(bsc, bi, brk, n0, i0, 0u);
                 lex_update(bsc, bi, brk, n1, i1, 0u);
             }
+            auto pairv = [&](const Pair2<A> b) {  // a partner's record (32-bit sums)
+                r0 = min(r0, score4((uint32_t)se0, (uint32_t)sl0, (uint32_t)pe0, (uint32_t)pl0, (uint32_t)b.a,
+                                    (uint32_t)b.b));
+                r1 = min(r1, score4((uint32_t)se1, (uint32_t)sl1, (uint32_t)pe1, (uint32_t)pl1, (uint32_t)b.a,
+                                    (uint32_t)b.b));
+            };
             auto pair = [&](uint32_t pj) {
                 const Pair2<A> b = T.el(pj);
                 if (sizeof(A) == 4) {
@@ -932,25 +949,43 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 }
             };
             uint32_t v = 0;
-            for (; v + 4 <= nBs; v += 4) {
-                const uint32_t q0 = lp[v], q1 = lp[v + 1], q2 = lp[v + 2], q3 = lp[v + 3];
-                pair(q0);
-                pair(q1);
-                pair(q2);
-                pair(q3);
+            if constexpr (sizeof(A) == 4) {
+                if constexpr (gath) {  // two partners per 16-byte load
+                    const uint4* l4 = reinterpret_cast<const uint4*>(lp8);
+                    for (; v + 4 <= nBs; v += 4) {
+                        const uint4 x = l4[v / 2], y = l4[v / 2 + 1];
+                        pairv(Pair2<A>{x.x, x.y});
+                        pairv(Pair2<A>{x.z, x.w});
+                        pairv(Pair2<A>{y.x, y.y});
+                        pairv(Pair2<A>{y.z, y.w});
+                    }
+                    for (; v < nBs; ++v) pairv(lp8[v]);
+                }
             }
-            for (; v < nBs; ++v) pair(lp[v]);
-            for (v = cap; v + 4 <= nB; v += 4) {
-                const uint32_t q0 = __ldcg(gsp + v), q1 = __ldcg(gsp + v + 1);
-                const uint32_t q2 = __ldcg(gsp + v + 2), q3 = __ldcg(gsp + v + 3);
-                pair(q0);
-                pair(q1);
-                pair(q2);
-                pair(q3);
+            if constexpr (!gath) {
+                for (; v + 4 <= nBs; v += 4) {
+                    const uint32_t q0 = lp[v], q1 = lp[v + 1], q2 = lp[v + 2], q3 = lp[v + 3];
+                    pair(q0);
+                    pair(q1);
+                    pair(q2);
+                    pair(q3);
+                }
+                for (; v < nBs; ++v) pair(lp[v]);
             }
-            for (v = max(v, cap); v < nB; ++v) pair(__ldcg(gsp + v));
             if (sizeof(A) == 4)  // (row minimum, item): lexicographic over the lane's rows
                 bkey = min(bkey, min(pack64(r0, i0), pack64(r1, i1)));
+        }
+        p0 += cap;
+        if (!__any_sync(FULL, p0 < nB)) break;  // warp-uniform
+        __syncwarp(FULL);
+        {
+            const uint32_t nb = p0 < nB ? min(cap, nB - p0) : 0u;
+            if (gath)
+                for (uint32_t u = gl; u < nb; u += GL) lp8[u] = T.el(__ldcg(gsp + p0 + u));
+            else
+                for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + p0 + u);
+        }
+        __syncwarp(FULL);
         }
         ph.mark(3);
         if (sizeof(A) == 4) {
@@ -962,24 +997,30 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             const bool need = apply && bkey != ~0ull && (A)(bkey >> 32) < Ws;
             if (__any_sync(FULL, need)) {  // warp-uniform (the reduction below shuffles)
                 const uint32_t S = (uint32_t)(bkey >> 32), istar = (uint32_t)bkey;
-                uint32_t rb = 0xFFFFFFFFu;
+                // (rank << 32 | list index v): the apply step edits entry v of j''s list directly
+                u64 rv = ~0ull;
                 if (need) {
                     const Pair2<A> a = T.el(__ldg(p.item_pos + istar));
                     const A se = Bs.a - a.a, sl = Bs.b - a.b, pe = Bp.a + a.a, pl = Bp.b + a.b;
-                    if (gl == 0 && (uint32_t)maxa(maxa(se, sl), maxa(pe, pl)) == S) rb = 0;
+                    if (gl == 0 && (uint32_t)maxa(maxa(se, sl), maxa(pe, pl)) == S) rv = 0xFFFFFFFFull;
                     for (uint32_t v = gl; v < nB; v += GL) {
-                        const uint32_t pj = v < cap ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v);
-                        const Pair2<A> b = T.el(pj);
+                        const bool sm = v < cap && one_chunk;
+                        const uint32_t pj = (sm && gath) ? 0u : (sm ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v));
+                        const Pair2<A> b = (sm && gath) ? lp8[v] : T.el(pj);
                         const A sc = maxa(maxa<A>(se + b.a, sl + b.b), maxa<A>(pe - b.a, pl - b.b));
-                        if ((uint32_t)sc == S) rb = min(rb, T.idx(pj) + 1u);
+                        if ((uint32_t)sc == S) {
+                            const uint32_t rk = T.idx((sm && gath) ? (uint32_t)__ldcg(gsp + v) : pj) + 1u;
+                            rv = min(rv, ((u64)rk << 32) | v);
+                        }
                     }
                 }
 #pragma unroll
-                for (int off = GL / 2; off > 0; off >>= 1) rb = min(rb, __shfl_xor_sync(FULL, rb, off));
+                for (int off = GL / 2; off > 0; off >>= 1) rv = min(rv, __shfl_xor_sync(FULL, rv, off));
                 if (need) {
                     bsc = (A)S;
                     bi = istar;
-                    brk = rb;
+                    brk = (uint32_t)(rv >> 32);
+                    vstar = (uint32_t)rv;
                 }
             }
         } else {
@@ -998,9 +1039,11 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                         gss[u] = (uint16_t)(brk != 0u ? pj : last);
                     }
                 }
-                if (brk != 0u) {  // i' leaves j''s list, i takes its entry
+                if (brk != 0u && sizeof(A) == 4) {  // i' leaves j''s list (entry vstar), i takes it
+                    if (gl == 0) gsp[vstar] = (uint16_t)pi;
+                } else if (brk != 0u) {
                     for (uint32_t v = gl; v < nB; v += GL) {
-                        const uint32_t q = v < cap ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v);
+                        const uint32_t q = (v < cap && one_chunk) ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v);
                         if (q == pj) gsp[v] = (uint16_t)pi;
                     }
                 } else if (gl == 0) {
@@ -1011,7 +1054,21 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             } else {
                 dirty = true;
             }
-            if (gl == 0) {
+            if (gl == 0 && gath) {  // FL is formed after the refinement
+                const Pair2<A> a = T.el(pi);
+                Pair2<A> es = EL[js], ep = EL[jp];
+                es.a -= a.a; es.b -= a.b;
+                ep.a += a.a; ep.b += a.b;
+                set_apos(apos, pi, jp, wide);
+                if (brk != 0u) {
+                    const Pair2<A> b = T.el(pj);
+                    ep.a -= b.a; ep.b -= b.b;
+                    es.a += b.a; es.b += b.b;
+                    set_apos(apos, pj, js, wide);
+                }
+                EL[js] = es;
+                EL[jp] = ep;
+            } else if (gl == 0) {
                 const ItemRec<A> a = T.item(pi);
                 const A ae = a.e, al = a.l;
                 Pair2<A> es = EL[js], fs = FL[js], ep = EL[jp], fp = FL[jp];
@@ -1218,28 +1275,32 @@ DFLOP_DEV u64 score_order4(const CandParams& p, uint32_t sh, const Pair2<A>* EL,
     return T;
 }
 
-template <typename A, bool PK, int GL, bool SM, bool O4>
+template <typename A, bool PK, int GL, bool SM, bool O4, int MODE>
 DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, uint32_t co, Pair2<A>* EL,
                              Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, u64& Tc,
                              u64& cmax, PhaseTimer& ph, bool forced) {
     const uint32_t m = p.m;
-    bool from_lpt = false;
-    if constexpr (PK && sizeof(A) == 4) from_lpt = p.lpt_in != 0;
-    if (from_lpt) {
+    if constexpr (MODE != 0) {
         // split pipeline: k_lpt left this candidate's packed bucket keys (offset removed) and
         // its assignment; the caller copied the assignment into apos
         const uint2* src = reinterpret_cast<const uint2*>(p.lpt_el) + (size_t)(c - p.c_begin) * m;
+        constexpr bool gath = MODE == 2;  // FL shares the scratch: formed after the refinement
         for (uint32_t j = gl; j < m; j += GL) {
             const uint2 v = __ldcg(src + j);
             EL[j] = Pair2<A>{(A)v.x, (A)v.y};
-            FL[j] = Pair2<A>{0, 0};
+            if (!gath) FL[j] = Pair2<A>{0, 0};
         }
         __syncwarp(FULL);
         ph.mark(0);
         if (m >= 2 && p.R > 0)
-            refine<A, PK, GL, SM>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
-        else
+            refine<A, PK, GL, SM, gath>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
+        if (gath || !(m >= 2 && p.R > 0)) {
+            if (gath) {
+                for (uint32_t j = gl; j < m; j += GL) FL[j] = Pair2<A>{0, 0};
+                __syncwarp(FULL);
+            }
             form_fl<A, GL, SM>(p, T, apos, p.wide != 0, FL, gl);
+        }
     } else {
     for (uint32_t j = gl; j < m; j += GL) {
         // co: the LPT probe offset; the plain variant's lane-local LPT keys carry k = j / GL
@@ -1296,7 +1357,9 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
     ph.mark(5);
 }
 
-template <typename A, bool PK, int GL, bool SM, bool O4>
+// MODE 0: the whole candidate (LPT, refinement, 1F1B); 1: the split pipeline's second kernel
+// (from k_lpt's output: refinement + 1F1B; packed u32 only); 2: the same in gather mode
+template <typename A, bool PK, int GL, bool SM, bool O4, int MODE = 0>
 __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     if (p.hdr->variant != p.want_variant) return;  // another variant runs
     uint32_t sh = PK ? p.hdr->shift : 0u;
@@ -1383,14 +1446,14 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
         if (!__any_sync(FULL, valid)) break;  // warp-uniform: every group of the warp is done
         const uint32_t c = valid ? cc : p.c_end - 1;  // tail groups recompute a real candidate
         uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
-        if (PK && sizeof(A) == 4 && p.lpt_in) {  // the chunk's assignment from k_lpt into the slot's working buffer
+        if constexpr (MODE != 0) {  // the chunk's assignment from k_lpt into the slot's working buffer
             const uint4* src = reinterpret_cast<const uint4*>(p.lpt_apos + (size_t)(c - p.c_begin) * p.apos_bytes);
             uint4* dst = reinterpret_cast<uint4*>(apos);
             for (uint32_t b = gl; b < p.apos_bytes / 16; b += GL) dst[b] = __ldcg(src + b);
             __syncwarp(FULL);
         }
         u64 Tc, cmax;
-        run_candidate<A, PK, GL, SM, O4>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph, forced);
+        run_candidate<A, PK, GL, SM, O4, MODE>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph, forced);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
         u64 key;
         if (Tc >= (1ull << 40)) {
@@ -1506,6 +1569,37 @@ static void launch_gl(const CandLaunch& L, const CandParams& p, cudaStream_t s) 
         default: k_candidates<A, PK, 32, SM, O4><<<grid, block, L.dyn, s>>>(p); break;
     }
 }
+
+// the split pipeline's candidate kernel (packed u32, shared-memory table; m >= 48: GL >= 8)
+template <bool O4, int MODE>
+static const void* ptr_split_gl(int gl) {
+    switch (gl) {
+        case 8: return reinterpret_cast<const void*>(&k_candidates<uint32_t, true, 8, true, O4, MODE>);
+        case 16: return reinterpret_cast<const void*>(&k_candidates<uint32_t, true, 16, true, O4, MODE>);
+        default: return reinterpret_cast<const void*>(&k_candidates<uint32_t, true, 32, true, O4, MODE>);
+    }
+}
+
+template <bool O4, int MODE>
+static void launch_split_gl(const CandLaunch& L, const CandParams& p, cudaStream_t s) {
+    const dim3 grid(L.grid), block(L.cpb * L.gl);
+    switch (L.gl) {
+        case 8: k_candidates<uint32_t, true, 8, true, O4, MODE><<<grid, block, L.dyn, s>>>(p); break;
+        case 16: k_candidates<uint32_t, true, 16, true, O4, MODE><<<grid, block, L.dyn, s>>>(p); break;
+        default: k_candidates<uint32_t, true, 32, true, O4, MODE><<<grid, block, L.dyn, s>>>(p); break;
+    }
+}
+
+#define DFLOP_SPLIT_UNIT(NAME, O4)                                                               \
+    const void* split_ptr_##NAME(int mode, int gl) {                                              \
+        return mode == 2 ? ptr_split_gl<O4, 2>(gl) : ptr_split_gl<O4, 1>(gl);                     \
+    }                                                                                             \
+    void split_launch_##NAME(int mode, const CandLaunch& L, const CandParams& p, cudaStream_t s) { \
+        if (mode == 2)                                                                            \
+            launch_split_gl<O4, 2>(L, p, s);                                                      \
+        else                                                                                      \
+            launch_split_gl<O4, 1>(L, p, s);                                                      \
+    }
 
 // one translation unit per (variant, table placement, ORDER4) so the 72 instantiations build
 // in parallel

@@ -90,6 +90,7 @@ struct BalanceConfig {
     // split pipeline (packed variant only): k_lpt with lpt_gl lanes per candidate, then the
     // candidate kernel on its output, over chunks of lpt_chunk candidates
     bool split = false;
+    bool gather = false;               // CandParams::gather for the split candidate kernel
     int lpt_gl = 0;
     uint32_t lpt_cpb = 0, lpt_grid = 0, lpt_tbl = 0, lpt_cb = 0, lpt_chunk = 0;
     // workspace layout (byte offsets)

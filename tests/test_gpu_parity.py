@@ -190,10 +190,12 @@ def test_balance_shard_window_config5(D, O, presets):
     (2500, 250, 1, 5000),     # m = 250: GL = 4, generic
     (40, 64, 1, 2 ** 20),     # n < m
 ])
-def test_split_pipeline_parity(D, O, presets, monkeypatch, n, n_mb, l_dp, hi):
+@pytest.mark.parametrize("gather", ["0", "1"])
+def test_split_pipeline_parity(D, O, presets, monkeypatch, n, n_mb, l_dp, hi, gather):
     """The split pipeline (k_lpt, then the candidate kernel from its output)
-    forced on (DFLOP_SPLIT=2) over several chunks: every candidate equals the merged kernel's
-    (DFLOP_SPLIT=0) and, on a window, the oracle's."""
+    forced on (DFLOP_SPLIT=2) over several chunks, with and without the gather mode: every
+    candidate equals the merged kernel's (DFLOP_SPLIT=0) and, on a window, the oracle's."""
+    monkeypatch.setenv("DFLOP_SPLIT_GATHER", gather)
     p = presets[5]
     if hi is None:
         q = O.predict(p.model, p.plan, *p.features(1))[1]
