@@ -803,7 +803,9 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
 // ---------------------------------------------------------------- swap refinement (O6)
 // `apply` is false for c < 2: the rounds are still executed (and discarded) so that every
 // group of a warp issues the same shuffle sequence.
-template <typename A, bool PK, int GL, bool SM, bool GA = false>
+// CS: the counters are known to be in shared memory (the split kernel: m <= 255) -- shared
+// atomics instead of generic ones
+template <typename A, bool PK, int GL, bool SM, bool GA = false, bool CS = false>
 DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
                       uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, bool apply, PhaseTimer& ph) {
     const uint32_t m = p.m, cap = p.cap;
@@ -813,7 +815,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
     // members of j* (ls) and j' (lp)
     uint32_t* cnt;
     uint16_t* ls;
-    if (p.cnt_smem) {
+    if (CS || p.cnt_smem) {
         cnt = reinterpret_cast<uint32_t*>(scr);
         ls = reinterpret_cast<uint16_t*>(cnt + 2 * m + 1);
     } else {
@@ -1293,7 +1295,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         __syncwarp(FULL);
         ph.mark(0);
         if (m >= 2 && p.R > 0)
-            refine<A, PK, GL, SM, gath>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
+            refine<A, PK, GL, SM, gath, true>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
         if (gath || !(m >= 2 && p.R > 0)) {
             if (gath) {
                 for (uint32_t j = gl; j < m; j += GL) FL[j] = Pair2<A>{0, 0};
