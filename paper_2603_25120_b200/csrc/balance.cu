@@ -557,6 +557,36 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         cudaFuncSetAttribute(split_kernel_ptr(cfg.gather ? 2 : 1, gl, (sh.mode & DFLOP_MODE_ORDER4) != 0),
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)((size_t)cfg.tbl_bytes[0] + (size_t)cfg.cpb[0] * cfg.cand_bytes[0]));
+        // fused pipeline (k_fused): one persistent CTA per SM whose warps take LPT tasks (16
+        // candidates, 2 lanes each) or refinement tasks (32 / gl candidates) -- the region of
+        // a warp holds either layout
+        if (env_int("DFLOP_FUSED", 0) != 0 && !cfg.gather) {
+            uint32_t fl = round16(m * 8u) + 16u;
+            while (fl % 128 != 16) fl += 16;
+            const uint32_t region = std::max(16u * fl, (32u / (uint32_t)gl) * cfg.cand_bytes[0]);
+            // the ring (per CTA): twice the LPT candidates its warps can hold; its flags (and
+            // 16 bytes of counters) in shared memory after the warp regions
+            uint32_t nw = (uint32_t)std::min<size_t>(kFusedMaxThreads / 32, (smem_max - cfg.tbl_bytes[0]) / region);
+            auto ring_of = [&](uint32_t w) {
+                const int fr = env_int("DFLOP_FUSED_RING", 0);
+                return fr >= 32 ? (uint32_t)fr : 2u * w * 16u;
+            };
+            while (nw >= 2 &&
+                   (size_t)cfg.tbl_bytes[0] + (size_t)nw * region + 16 + 8 * (size_t)ring_of(nw) > smem_max)
+                --nw;
+            if (nw >= 2) {
+                cfg.fused = true;
+                cfg.fz_warps = nw;
+                cfg.fz_region = region;
+                cfg.fz_lcb = fl;
+                cfg.fz_ring = ring_of(nw);
+                cfg.lpt_chunk = nsm * (cfg.fz_ring + 1) - 1;  // the rings live in the split pipeline's buffers
+                cfg.n_slots = std::max(cfg.n_slots, nsm * nw * (32u / (uint32_t)gl));
+                cudaFuncSetAttribute(fused_kernel_ptr(gl, (sh.mode & DFLOP_MODE_ORDER4) != 0),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((size_t)cfg.tbl_bytes[0] + (size_t)nw * region + 16 + 8 * cfg.fz_ring));
+            }
+        }
     }
     if (env_int("DFLOP_DEBUG", 0))
         fprintf(stderr,
@@ -586,6 +616,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         cfg.o_lpt_apos = o;  o += align256(((size_t)cfg.lpt_chunk + 1) * cfg.apos_bytes);
         cfg.o_lpt_el = o;    o += align256(((size_t)cfg.lpt_chunk + 1) * m * 8);
     }
+
     cfg.total = o;
     cfg.ok = true;
     return cfg;
@@ -680,7 +711,29 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
         cudaFuncSetAttribute(cand_kernel_ptr(v, cfg.gl, cfg.tbl_smem[v], p.order4 != 0),
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)L.dyn);
-        if (v == 0 && cfg.split) {
+        if (v == 0 && cfg.fused) {
+            // one persistent launch over [c_begin, c_end) (k_fused_init resets its counters)
+            CandParams qf = q;
+            qf.lpt_apos = reinterpret_cast<uint8_t*>(ws + cfg.o_lpt_apos);
+            qf.lpt_el = reinterpret_cast<uint32_t*>(ws + cfg.o_lpt_el);
+            qf.lpt_in = 1;
+            FusedParams f{};
+            f.ring = cfg.fz_ring;
+            f.region = cfg.fz_region;
+            f.lpt_cb = cfg.fz_lcb;
+            f.lpt_off_stage = round16(a.sh.m * 8u);
+            const int rw = env_int("DFLOP_FUSED_REF", 0);
+            f.ref_warps = rw > 0 ? (uint32_t)rw : cfg.fz_warps / 2;
+            f.spin_limit = 1u << 24;
+            f.roles = env_int("DFLOP_FUSED_ROLES", 0) != 0 ? 1u : 0u;
+            const size_t dyn = (size_t)cfg.tbl_bytes[0] + (size_t)cfg.fz_warps * cfg.fz_region + 16 + 8 * cfg.fz_ring;
+            cudaFuncSetAttribute(fused_kernel_ptr(cfg.gl, p.order4 != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dyn);
+            int dev = 0;
+            cudaGetDevice(&dev);
+            const uint32_t nsm = (uint32_t)dev_attr(dev).sms;
+            fused_launch(cfg.gl, nsm, cfg.fz_warps * 32, dyn, qf, f, s);
+        } else if (v == 0 && cfg.split) {
             // per chunk: k_lpt, then the packed candidate kernel on its output (both return at
             // once when another variant runs)
             CandParams ql = q;

@@ -1280,12 +1280,12 @@ DFLOP_DEV u64 score_order4(const CandParams& p, uint32_t sh, const Pair2<A>* EL,
 template <typename A, bool PK, int GL, bool SM, bool O4, int MODE>
 DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, uint32_t co, Pair2<A>* EL,
                              Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, u64& Tc,
-                             u64& cmax, PhaseTimer& ph, bool forced) {
+                             u64& cmax, PhaseTimer& ph, bool forced, uint32_t ent = 0) {
     const uint32_t m = p.m;
     if constexpr (MODE != 0) {
         // split pipeline: k_lpt left this candidate's packed bucket keys (offset removed) and
         // its assignment; the caller copied the assignment into apos
-        const uint2* src = reinterpret_cast<const uint2*>(p.lpt_el) + (size_t)(c - p.c_begin) * m;
+        const uint2* src = reinterpret_cast<const uint2*>(p.lpt_el) + (size_t)ent * m;  // k_lpt's entry
         constexpr bool gath = MODE == 2;  // FL shares the scratch: formed after the refinement
         for (uint32_t j = gl; j < m; j += GL) {
             const uint2 v = __ldcg(src + j);
@@ -1455,7 +1455,8 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
             __syncwarp(FULL);
         }
         u64 Tc, cmax;
-        run_candidate<A, PK, GL, SM, O4, MODE>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph, forced);
+        run_candidate<A, PK, GL, SM, O4, MODE>(p, T, c, sh, co, EL, FL, apos, scr, csr, gl, Tc, cmax, ph, forced,
+                                                c - p.c_begin);
         Tc = __shfl_sync(FULL, Tc, 0, GL);
         u64 key;
         if (Tc >= (1ull << 40)) {
@@ -1544,6 +1545,222 @@ __global__ void __launch_bounds__(kLptMaxThreads) k_lpt(CandParams p) {
             __stcg(reinterpret_cast<unsigned long long*>(dst + j), pack64(x.b - co, x.a));
         }
         __syncwarp(FULL);
+    }
+}
+
+// ---------------------------------------------------------------- fused pipeline: one kernel
+// The split pipeline's two stages in one persistent kernel.  CTA b owns
+// the candidates [c_begin + b*Q, c_begin + (b+1)*Q) and a ring of f.ring global entries
+// (assignment + packed bucket keys).  Every warp owns f.region bytes of shared memory and
+// repeatedly takes either an LPT task (16 consecutive candidates, 2 lanes each, as k_lpt) or
+// a refinement task (RG = 32 / GLR consecutive candidates whose LPT is done: refinement and
+// 1F1B from the entry, as the split candidate kernel), so the SM's warps mix the ALU-bound
+// LPT with the latency- and shared-memory-bound refinement.  Scheduling state lives in shared
+// memory: the two claim counters, the number of warps refining, and per ring entry done[e] =
+// c + 1 (LPT of c written; the writer fences at GPU scope first, the entry is read from L2)
+// and used[e] = c + 1 (consumed).  A task is claimed with atomicCAS only once it is ready,
+// so no warp ever waits on a claimed task and the kernel cannot deadlock; a warp with
+// nothing to do sleeps briefly and gives up with DFLOP_DEV_PIPELINE_ERROR after
+// f.spin_limit empty polls (a safety net, never expected).  Policy: refine when a task is
+// ready and fewer than f.ref_warps warps refine (or no LPT task can start), else LPT.
+template <int GLR, bool O4>
+__global__ void __launch_bounds__(kFusedMaxThreads) k_fused(CandParams p, FusedParams f) {
+    if (p.hdr->variant != 0) return;  // the packed variant only
+    const uint32_t sh = p.hdr->shift, co = p.hdr->offs;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t nw = blockDim.x >> 5;
+    uint32_t* sched = reinterpret_cast<uint32_t*>(smem + p.tbl_bytes + (size_t)nw * f.region);
+    volatile uint32_t* vs = sched;  // [0] next LPT, [1] next refinement, [2] warps refining
+    volatile uint32_t* done = sched + 4;
+    volatile uint32_t* used = sched + 4 + f.ring;
+    const uint32_t Q = (p.c_end - p.c_begin + gridDim.x - 1) / gridDim.x;
+    const uint32_t cb = min(p.c_end, p.c_begin + blockIdx.x * Q), ce = min(p.c_end, cb + Q);
+    Tbl<uint32_t, true> T;
+    {
+        const uint32_t words = p.n * (uint32_t)sizeof(ItemRec<uint32_t>) / 16;
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
+            reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.items) + i);
+        uint16_t* pi16 = reinterpret_cast<uint16_t*>(smem + (size_t)p.n * sizeof(ItemRec<uint32_t>));
+        for (uint32_t i = threadIdx.x; i < p.n; i += blockDim.x) pi16[i] = (uint16_t)__ldg(p.pos_item + i);
+        for (uint32_t i = threadIdx.x; i < 4 + 2 * f.ring; i += blockDim.x) sched[i] = i < 2 ? cb : 0u;
+        __syncthreads();
+        T.it = reinterpret_cast<const ItemRec<uint32_t>*>(smem);
+        T.it_s = (uint32_t)__cvta_generic_to_shared(smem);
+        T.pi16 = pi16;
+        T.pi32 = nullptr;
+    }
+    bool forced = false;  // as in k_candidates
+    if (p.m >= 1 && p.m <= p.n) {
+        bool ok = true;
+        for (uint32_t q = threadIdx.x & 31u; q < p.m; q += 32) {
+            const Pair2<uint32_t> r = T.el(q);
+            ok = ok && r.a != 0 && r.b != 0;
+        }
+        forced = __all_sync(FULL, ok);
+    }
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5, m = p.m;
+    uint8_t* region = smem + p.tbl_bytes + (size_t)w * f.region;
+    // this CTA's ring: entries e + blockIdx.x * (ring + 1), the last one scratch
+    const size_t ring0 = (size_t)blockIdx.x * (f.ring + 1);
+    // refinement role: RG groups of GLR lanes, one persistent slot each
+    constexpr uint32_t RG = 32u / GLR;
+    const uint32_t rg = lane / GLR, rgl = lane % GLR;
+    const uint32_t slot = (blockIdx.x * nw + w) * RG + rg;
+    uint8_t* bufs = p.slot_apos + (size_t)slot * 2 * p.apos_bytes;
+    uint16_t* csr = p.slot_csr + (size_t)slot * p.csr_len;
+    for (uint32_t b = p.n + rgl; b < p.apos_bytes; b += GLR) {  // padding past n: never a bucket
+        bufs[b] = 0xFF;
+        bufs[p.apos_bytes + b] = 0xFF;
+    }
+    __syncwarp(FULL);
+    u64 best_key = p.slot_key[slot], best_T = 0, best_cmax = 0;
+    uint32_t best_buf = 0;
+    if (best_key != ~0ull) {
+        best_T = p.slot_T[slot];
+        best_cmax = p.slot_cmax[slot];
+        best_buf = p.slot_buf[slot];
+    }
+    uint32_t cur = best_buf ^ 1u;
+    // LPT role: 16 groups of 2 lanes
+    const uint32_t lg = lane >> 1, lgl = lane & 1u;
+    PhaseTimer ph;
+    ph.start(nullptr);
+    uint32_t idle = 0;
+    for (;;) {
+        uint32_t task = 0, arg = 0;  // 1: refinement of [arg, arg + RG), 2: LPT of [arg, arg + 16), 3: exit
+        if (lane == 0) {
+            const uint32_t r = vs[1], l = vs[0];
+            bool ready = r < ce;
+            const uint32_t re = min(r + RG, ce);
+            for (uint32_t c = r; c < re && ready; ++c) ready = done[(c - cb) % f.ring] == c + 1;
+            const uint32_t le = min(l + 16u, ce);
+            bool lpt_ok = l < ce;  // the ring entries' previous candidates are consumed
+            for (uint32_t c = l; c < le && lpt_ok; ++c)
+                if (c - cb >= f.ring) lpt_ok = used[(c - cb) % f.ring] == c - f.ring + 1;
+            if (f.roles) {  // fixed roles by scheduler: SMSPs 0, 1 run the LPT, 2, 3 refine
+                if ((w & 3u) < 2u)
+                    ready = false;
+                else
+                    lpt_ok = false;
+            }
+            const bool ref_first = ready && (vs[2] < f.ref_warps || !lpt_ok);
+            if (ref_first && atomicCAS(sched + 1, r, re) == r) {
+                task = 1;
+                arg = r;
+            } else if (lpt_ok && atomicCAS(sched, l, le) == l) {
+                task = 2;
+                arg = l;
+            } else if (ready && atomicCAS(sched + 1, r, re) == r) {
+                task = 1;
+                arg = r;
+            } else if (r >= ce && l >= ce) {
+                task = 3;
+            }
+            if (task == 1) atomicAdd(sched + 2, 1u);
+            if (task == 0 && ++idle > f.spin_limit) {
+                atomicOr(&p.hdr->status, (uint32_t)DFLOP_DEV_PIPELINE_ERROR);
+                task = 3;
+            }
+        }
+        task = __shfl_sync(FULL, task, 0);
+        arg = __shfl_sync(FULL, arg, 0);
+        __syncwarp(FULL);
+        if (task == 3) break;
+        if (task == 0) {
+            __nanosleep(64);
+            continue;
+        }
+        idle = 0;
+        if (task == 2) {
+            const uint32_t cc = arg + lg;
+            const bool valid = cc < arg + 16u && cc < ce;
+            const uint32_t c = valid ? cc : ce - 1;                     // tail groups recompute a real candidate
+            const uint32_t e = valid ? (cc - cb) % f.ring : f.ring;     // ... into the scratch entry
+            Pair2<uint32_t>* EL = reinterpret_cast<Pair2<uint32_t>*>(region + (size_t)lg * f.lpt_cb);
+            uint8_t* stage = region + (size_t)lg * f.lpt_cb + f.lpt_off_stage;
+            uint8_t* apos = p.lpt_apos + (ring0 + e) * p.apos_bytes;
+            for (uint32_t j = lgl; j < m; j += 2) EL[j] = Pair2<uint32_t>{j, j + co};
+            for (uint32_t b = p.n + lgl; b < p.apos_bytes; b += 2) apos[b] = 0xFF;
+            __syncwarp(FULL);
+            lpt_pass<uint32_t, true, 2, true>(p, T, c, sh, EL, EL, apos, stage, lgl, co, forced);
+            Pair2<uint32_t>* dst = reinterpret_cast<Pair2<uint32_t>*>(p.lpt_el) + (ring0 + e) * m;
+            for (uint32_t j = lgl; j < m; j += 2) {
+                const Pair2<uint32_t> x = EL[j];
+                __stcg(reinterpret_cast<unsigned long long*>(dst + j), pack64(x.b - co, x.a));
+            }
+            __threadfence();  // the entry reaches L2 before its flag
+            __syncwarp(FULL);
+            if (lgl == 0 && valid) done[e] = c + 1;
+        } else {
+            const uint32_t cc = arg + rg;
+            const bool valid = cc < ce;
+            const uint32_t c = valid ? cc : ce - 1;
+            const uint32_t e = (c - cb) % f.ring;
+            uint8_t* base = region + (size_t)rg * p.cand_bytes;
+            Pair2<uint32_t>* EL = reinterpret_cast<Pair2<uint32_t>*>(base);
+            Pair2<uint32_t>* FL = reinterpret_cast<Pair2<uint32_t>*>(base + p.off_fl);
+            uint8_t* scr = base + p.off_scr;
+            uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
+            {
+                const uint4* src = reinterpret_cast<const uint4*>(p.lpt_apos + (ring0 + e) * p.apos_bytes);
+                uint4* dst = reinterpret_cast<uint4*>(apos);
+                for (uint32_t b = rgl; b < p.apos_bytes / 16; b += GLR) dst[b] = __ldcg(src + b);
+                __syncwarp(FULL);
+            }
+            u64 Tc, cmax;
+            run_candidate<uint32_t, true, GLR, true, O4, 1>(p, T, c, sh, co, EL, FL, apos, scr, csr, rgl, Tc, cmax,
+                                                             ph, forced, (uint32_t)(ring0 + e));
+            __syncwarp(FULL);
+            if (rgl == 0 && valid) used[e] = c + 1;  // the entry may be reused
+            if (lane == 0) atomicSub(sched + 2, 1u);
+            Tc = __shfl_sync(FULL, Tc, 0, GLR);
+            u64 key;
+            if (Tc >= (1ull << 40)) {
+                if (rgl == 0) atomicOr(&p.hdr->status, (uint32_t)DFLOP_DEV_MAKESPAN_OVERFLOW);
+                key = (((1ull << 40) - 1) << 24) | (u64)(p.id_base + c);
+            } else {
+                key = (Tc << 24) | (u64)(p.id_base + c);
+            }
+            if (valid) {
+                if (rgl == 0 && p.cand_T) {
+                    p.cand_T[c - p.c_begin] = Tc;
+                    p.cand_cmax[c - p.c_begin] = cmax;
+                }
+                if (key < best_key) {
+                    best_key = key;
+                    best_T = Tc;
+                    best_cmax = cmax;
+                    best_buf = cur;
+                    cur ^= 1u;
+                }
+            }
+        }
+    }
+    if (rgl == 0) {
+        p.slot_key[slot] = best_key;
+        p.slot_T[slot] = best_T;
+        p.slot_cmax[slot] = best_cmax;
+        p.slot_buf[slot] = best_buf;
+        if (best_key != ~0ull) atomicMin(&p.hdr->best_key, best_key);
+    }
+}
+
+template <bool O4>
+static const void* ptr_fused_gl(int gl) {
+    switch (gl) {
+        case 8: return reinterpret_cast<const void*>(&k_fused<8, O4>);
+        case 16: return reinterpret_cast<const void*>(&k_fused<16, O4>);
+        default: return reinterpret_cast<const void*>(&k_fused<32, O4>);
+    }
+}
+
+template <bool O4>
+static void launch_fused_gl(int gl, uint32_t grid, uint32_t threads, size_t dyn, const CandParams& p,
+                            const FusedParams& f, cudaStream_t s) {
+    switch (gl) {
+        case 8: k_fused<8, O4><<<grid, threads, dyn, s>>>(p, f); break;
+        case 16: k_fused<16, O4><<<grid, threads, dyn, s>>>(p, f); break;
+        default: k_fused<32, O4><<<grid, threads, dyn, s>>>(p, f); break;
     }
 }
 
