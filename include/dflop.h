@@ -54,8 +54,6 @@ typedef int32_t dflop_status;
 /* Device status word bits (written by kernels into a caller-provided u32). */
 #define DFLOP_DEV_COST_OVERFLOW 1u     /* a predicted cost rounded to >= 2^32 ticks  */
 #define DFLOP_DEV_MAKESPAN_OVERFLOW 2u /* a makespan >= 2^40 ticks (packed argmin key) */
-#define DFLOP_DEV_PIPELINE_ERROR 4u    /* internal: the fused candidate pipeline stopped
-                                          waiting for work (never expected; results invalid) */
 
 typedef void* dflop_stream_t; /* cudaStream_t */
 

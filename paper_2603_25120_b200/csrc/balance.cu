@@ -437,16 +437,12 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         uint32_t cb, tbl, cpb;
         bool tbl_smem;
     };
-    // gather mode of the split candidate kernel (CandParams::gather): FL shares the scratch
-    bool gat = split_pre && env_int("DFLOP_SPLIT_GATHER", 0) != 0;
     auto layout = [&](int v, uint32_t cap) {
         Lay L;
         const uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cap, rings));
         const uint32_t asz = v == 2 ? 8u : 4u;
         const uint32_t el = round16(m * 2u * asz);   // EL[m] then FL[m]
         uint32_t cb = 2 * el + scr;
-        if (v == 0 && gat)  // EL, then {cnt, off, ls, lp8} during the refinement / {rings, FL} after
-            cb = el + std::max(round16(4u * (2u * m + 1u) + 2u * cap) + 8u * cap, round16(rings) + el);
         // stagger consecutive candidates across banks: a group's probe touches GL*2*asz bytes
         uint32_t span = std::max(16u, (uint32_t)gl * 2u * asz);
         if (v == 0 && split_pre && stg_env >= 16 && stg_env < 128 && stg_env % 16 == 0) span = (uint32_t)stg_env;
@@ -458,7 +454,6 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         const uint32_t tbl = (uint32_t)(((size_t)n * (v == 2 ? 32u : 16u) + (size_t)n * 2 + 127) & ~(size_t)127);
         // stage the table in shared memory when it leaves room for at least 2 warps of candidates
         L.tbl_smem = (size_t)tbl + (size_t)2 * per_warp * cb <= smem_max;
-        if (v == 0 && split_pre && env_int("DFLOP_SPLIT_GTBL", 0)) L.tbl_smem = false;
         L.tbl = L.tbl_smem ? tbl : 0;
         uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - L.tbl) / cb, kCandMaxThreads / gl);
         // no more groups than the family needs (one CTA per SM), whole warps only
@@ -473,7 +468,6 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     // length, shrunk (not below 32) while that buys resident candidates -- occupancy hides the
     // latency of the shared-memory and shuffle chains (config 5: cap 128 -> 104 raises 72 -> 80
     // candidates per SM, -6.7%; 768-thread blocks would need <= 80 registers: +37%)
-    for (int attempt = 0; attempt < 2; ++attempt) {
     uint32_t cap = std::min(128u, std::max(32u, next_pow2(2 * std::max(1u, per_bucket))));
     {
         uint32_t best = cap, best_cpb = layout(0, cap).cpb;
@@ -497,10 +491,6 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         cfg.tbl_bytes[v] = L.tbl;
         cfg.off_fl[v] = round16(m * 2u * (v == 2 ? 8u : 4u));
         cfg.off_scr[v] = 2 * cfg.off_fl[v];
-        if (v == 0 && gat) {
-            cfg.off_scr[v] = cfg.off_fl[v];
-            cfg.off_fl[v] = cfg.off_scr[v] + round16(rings);
-        }
         if (cpb == 0) {
             char buf[200];
             snprintf(buf, sizeof buf,
@@ -517,17 +507,9 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         cfg.cpb[v] = cpb;
         cfg.grid[v] = std::max(1u, std::min<uint32_t>(want, nsm));
     }
-    // the gather layout only with the split pipeline (the merged kernel maintains FL)
-    if (gat && !(cfg.tbl_smem[0] || env_int("DFLOP_SPLIT_GTBL", 0))) {
-        gat = false;
-        continue;
-    }
-    break;
-    }
-    cfg.gather = gat;
     cfg.n_slots = 0;
     for (int v = 0; v < 3; ++v) cfg.n_slots = std::max(cfg.n_slots, cfg.grid[v] * cfg.cpb[v]);
-    if (split_pre && (cfg.tbl_smem[0] || env_int("DFLOP_SPLIT_GTBL", 0)) && cfg.cpb[0] > 0) {
+    if (split_pre && cfg.tbl_smem[0] && cfg.cpb[0] > 0) {
         // chunks of r LPT rounds, r chosen so that the candidate kernel's rounds over a chunk
         // are nearly whole
         const uint32_t wave = nsm * lcpb, res0 = cfg.grid[0] * cfg.cpb[0];
@@ -554,39 +536,9 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         if (fch > 0) cfg.lpt_chunk = std::min<uint32_t>(sh.n_cand, (uint32_t)fch);
         cudaFuncSetAttribute(lpt_kernel_ptr(lg), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)((size_t)ltbl + (size_t)lcpb * lcb));
-        cudaFuncSetAttribute(split_kernel_ptr(cfg.gather ? 2 : 1, gl, (sh.mode & DFLOP_MODE_ORDER4) != 0),
+        cudaFuncSetAttribute(split_kernel_ptr(gl, (sh.mode & DFLOP_MODE_ORDER4) != 0),
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)((size_t)cfg.tbl_bytes[0] + (size_t)cfg.cpb[0] * cfg.cand_bytes[0]));
-        // fused pipeline (k_fused): one persistent CTA per SM whose warps take LPT tasks (16
-        // candidates, 2 lanes each) or refinement tasks (32 / gl candidates) -- the region of
-        // a warp holds either layout
-        if (env_int("DFLOP_FUSED", 0) != 0 && !cfg.gather) {
-            uint32_t fl = round16(m * 8u) + 16u;
-            while (fl % 128 != 16) fl += 16;
-            const uint32_t region = std::max(16u * fl, (32u / (uint32_t)gl) * cfg.cand_bytes[0]);
-            // the ring (per CTA): twice the LPT candidates its warps can hold; its flags (and
-            // 16 bytes of counters) in shared memory after the warp regions
-            uint32_t nw = (uint32_t)std::min<size_t>(kFusedMaxThreads / 32, (smem_max - cfg.tbl_bytes[0]) / region);
-            auto ring_of = [&](uint32_t w) {
-                const int fr = env_int("DFLOP_FUSED_RING", 0);
-                return fr >= 32 ? (uint32_t)fr : 2u * w * 16u;
-            };
-            while (nw >= 2 &&
-                   (size_t)cfg.tbl_bytes[0] + (size_t)nw * region + 16 + 8 * (size_t)ring_of(nw) > smem_max)
-                --nw;
-            if (nw >= 2) {
-                cfg.fused = true;
-                cfg.fz_warps = nw;
-                cfg.fz_region = region;
-                cfg.fz_lcb = fl;
-                cfg.fz_ring = ring_of(nw);
-                cfg.lpt_chunk = nsm * (cfg.fz_ring + 1) - 1;  // the rings live in the split pipeline's buffers
-                cfg.n_slots = std::max(cfg.n_slots, nsm * nw * (32u / (uint32_t)gl));
-                cudaFuncSetAttribute(fused_kernel_ptr(gl, (sh.mode & DFLOP_MODE_ORDER4) != 0),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((size_t)cfg.tbl_bytes[0] + (size_t)nw * region + 16 + 8 * cfg.fz_ring));
-            }
-        }
     }
     if (env_int("DFLOP_DEBUG", 0))
         fprintf(stderr,
@@ -711,29 +663,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
         cudaFuncSetAttribute(cand_kernel_ptr(v, cfg.gl, cfg.tbl_smem[v], p.order4 != 0),
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)L.dyn);
-        if (v == 0 && cfg.fused) {
-            // one persistent launch over [c_begin, c_end) (k_fused_init resets its counters)
-            CandParams qf = q;
-            qf.lpt_apos = reinterpret_cast<uint8_t*>(ws + cfg.o_lpt_apos);
-            qf.lpt_el = reinterpret_cast<uint32_t*>(ws + cfg.o_lpt_el);
-            qf.lpt_in = 1;
-            FusedParams f{};
-            f.ring = cfg.fz_ring;
-            f.region = cfg.fz_region;
-            f.lpt_cb = cfg.fz_lcb;
-            f.lpt_off_stage = round16(a.sh.m * 8u);
-            const int rw = env_int("DFLOP_FUSED_REF", 0);
-            f.ref_warps = rw > 0 ? (uint32_t)rw : cfg.fz_warps / 2;
-            f.spin_limit = 1u << 24;
-            f.roles = env_int("DFLOP_FUSED_ROLES", 0) != 0 ? 1u : 0u;
-            const size_t dyn = (size_t)cfg.tbl_bytes[0] + (size_t)cfg.fz_warps * cfg.fz_region + 16 + 8 * cfg.fz_ring;
-            cudaFuncSetAttribute(fused_kernel_ptr(cfg.gl, p.order4 != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)dyn);
-            int dev = 0;
-            cudaGetDevice(&dev);
-            const uint32_t nsm = (uint32_t)dev_attr(dev).sms;
-            fused_launch(cfg.gl, nsm, cfg.fz_warps * 32, dyn, qf, f, s);
-        } else if (v == 0 && cfg.split) {
+        if (v == 0 && cfg.split) {
             // per chunk: k_lpt, then the packed candidate kernel on its output (both return at
             // once when another variant runs)
             CandParams ql = q;
@@ -745,9 +675,8 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
             q.lpt_apos = ql.lpt_apos;
             q.lpt_el = ql.lpt_el;
             q.lpt_in = 1;
-            q.gather = cfg.gather ? 1u : 0u;
             const size_t ldyn = (size_t)cfg.lpt_tbl + (size_t)cfg.lpt_cpb * cfg.lpt_cb;
-            cudaFuncSetAttribute(split_kernel_ptr(cfg.gather ? 2 : 1, cfg.gl, p.order4 != 0),
+            cudaFuncSetAttribute(split_kernel_ptr(cfg.gl, p.order4 != 0),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.dyn);
             cudaFuncSetAttribute(lpt_kernel_ptr(cfg.lpt_gl), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ldyn);
             for (uint32_t c0 = a.c_begin; c0 < a.c_end; c0 += cfg.lpt_chunk) {
@@ -758,7 +687,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
                     q.cand_cmax = p.cand_cmax + (c0 - a.c_begin);
                 }
                 lpt_launch(cfg.lpt_gl, cfg.lpt_grid, cfg.lpt_cpb, ldyn, ql, s);
-                split_launch(cfg.gather ? 2 : 1, L, q, s);
+                split_launch(L, q, s);
                 launches += 2;
             }
             launches -= 1;

@@ -54,11 +54,6 @@ struct CandParams {
     uint8_t* lpt_apos;
     uint32_t* lpt_el;
     uint32_t lpt_in;
-    // gather mode (split pipeline, 32-bit sums, m <= 256): each refinement round copies the
-    // (e, l) records of j''s first cap members into the scratch (lp8, 8 B each) so the pair
-    // search reads partners without table lookups; FL is not maintained during refinement but
-    // formed from the final assignment, in the scratch after the 1F1B rings (off_fl)
-    uint32_t gather;
 };
 
 struct CandLaunch {
@@ -71,27 +66,10 @@ struct CandLaunch {
 
 const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem, bool o4);
 void cand_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s);
-// the fused pipeline (k_fused, cand_impl.cuh): the split pipeline's two stages in one
-// persistent kernel, CTA-local scheduling in shared memory, hand-off through a per-CTA ring
-// of global entries (lpt_apos / lpt_el: gridDim.x * (ring + 1) entries, the last of each
-// CTA's range is scratch)
-struct FusedParams {
-    uint32_t ring;        // ring entries per CTA
-    uint32_t region;      // shared-memory bytes per warp (max of the two roles' layouts)
-    uint32_t lpt_cb;      // LPT role: bytes per candidate (keys, then the 16-byte stage)
-    uint32_t lpt_off_stage;
-    uint32_t ref_warps;   // policy: refine first while fewer warps refine
-    uint32_t spin_limit;  // empty polls before DFLOP_DEV_PIPELINE_ERROR
-    uint32_t roles;       // 1: fixed roles per scheduler (warp w % 4 < 2: LPT, else refinement)
-};
-constexpr int kFusedMaxThreads = 640;
-const void* fused_kernel_ptr(int gl, bool o4);
-void fused_launch(int gl, uint32_t grid, uint32_t threads, size_t dyn, const CandParams& p, const FusedParams& f,
-                  cudaStream_t s);
-// the split pipeline's candidate kernel (packed u32, shared-memory table, GL in {8, 16, 32});
-// mode 1: from k_lpt's output, mode 2: the same in gather mode (CandParams::gather)
-const void* split_kernel_ptr(int mode, int gl, bool o4);
-void split_launch(int mode, const CandLaunch& L, const CandParams& p, cudaStream_t s);
+// the split pipeline's candidate kernel (packed u32, shared-memory table, GL in {8, 16, 32}):
+// refinement and 1F1B from k_lpt's output
+const void* split_kernel_ptr(int gl, bool o4);
+void split_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 // the split pipeline's LPT kernel (packed u32 variant, item table in shared memory)
 constexpr int kLptMaxThreads = 640;
 const void* lpt_kernel_ptr(int gl);

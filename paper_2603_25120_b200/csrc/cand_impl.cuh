@@ -805,7 +805,7 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
 // group of a warp issues the same shuffle sequence.
 // CS: the counters are known to be in shared memory (the split kernel: m <= 255) -- shared
 // atomics instead of generic ones
-template <typename A, bool PK, int GL, bool SM, bool GA = false, bool CS = false>
+template <typename A, bool PK, int GL, bool SM, bool CS = false>
 DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL, Pair2<A>* FL,
                       uint8_t* apos, uint8_t* scr, uint16_t* csr, uint32_t gl, bool apply, PhaseTimer& ph) {
     const uint32_t m = p.m, cap = p.cap;
@@ -825,11 +825,8 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
     }
     uint32_t* off = cnt + m;
     uint16_t* lp = ls + cap;
-    // gather mode (CandParams::gather): j''s records instead of its positions, 16-byte aligned
-    constexpr bool gath = GA && sizeof(A) == 4;
-    Pair2<A>* lp8 = reinterpret_cast<Pair2<A>*>(scr + ((4u * (2u * m + 1u) + 2u * cap + 15u) & ~15u));
     bool dirty = true;  // the lists must be (re)built from the assignment
-    bool first = !gath;  // the first build also forms FL (LPT maintains EL only)
+    bool first = true;  // the first build also forms FL (LPT maintains EL only)
     for (uint32_t r = 0; r < p.R; ++r) {
         if (__any_sync(FULL, dirty)) {  // warp-uniform: a clean group rebuilds the same lists
             build_lists<A, GL, SM>(p, T, apos, wide, cnt, off, csr, gl, first ? FL : nullptr);
@@ -879,10 +876,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         {
             const uint32_t na = min(nA, cap), nb = min(nB, cap);
             for (uint32_t u = gl; u < na; u += GL) ls[u] = __ldcg(gss + u);
-            if (gath)
-                for (uint32_t u = gl; u < nb; u += GL) lp8[u] = T.el(__ldcg(gsp + u));
-            else
-                for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + u);
+            for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + u);
         }
         __syncwarp(FULL);
         ph.mark(2);
@@ -927,12 +921,6 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 lex_update(bsc, bi, brk, n0, i0, 0u);
                 lex_update(bsc, bi, brk, n1, i1, 0u);
             }
-            auto pairv = [&](const Pair2<A> b) {  // a partner's record (32-bit sums)
-                r0 = min(r0, score4((uint32_t)se0, (uint32_t)sl0, (uint32_t)pe0, (uint32_t)pl0, (uint32_t)b.a,
-                                    (uint32_t)b.b));
-                r1 = min(r1, score4((uint32_t)se1, (uint32_t)sl1, (uint32_t)pe1, (uint32_t)pl1, (uint32_t)b.a,
-                                    (uint32_t)b.b));
-            };
             auto pair = [&](uint32_t pj) {
                 const Pair2<A> b = T.el(pj);
                 if (sizeof(A) == 4) {
@@ -951,29 +939,14 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 }
             };
             uint32_t v = 0;
-            if constexpr (sizeof(A) == 4) {
-                if constexpr (gath) {  // two partners per 16-byte load
-                    const uint4* l4 = reinterpret_cast<const uint4*>(lp8);
-                    for (; v + 4 <= nBs; v += 4) {
-                        const uint4 x = l4[v / 2], y = l4[v / 2 + 1];
-                        pairv(Pair2<A>{x.x, x.y});
-                        pairv(Pair2<A>{x.z, x.w});
-                        pairv(Pair2<A>{y.x, y.y});
-                        pairv(Pair2<A>{y.z, y.w});
-                    }
-                    for (; v < nBs; ++v) pairv(lp8[v]);
-                }
+            for (; v + 4 <= nBs; v += 4) {
+                const uint32_t q0 = lp[v], q1 = lp[v + 1], q2 = lp[v + 2], q3 = lp[v + 3];
+                pair(q0);
+                pair(q1);
+                pair(q2);
+                pair(q3);
             }
-            if constexpr (!gath) {
-                for (; v + 4 <= nBs; v += 4) {
-                    const uint32_t q0 = lp[v], q1 = lp[v + 1], q2 = lp[v + 2], q3 = lp[v + 3];
-                    pair(q0);
-                    pair(q1);
-                    pair(q2);
-                    pair(q3);
-                }
-                for (; v < nBs; ++v) pair(lp[v]);
-            }
+            for (; v < nBs; ++v) pair(lp[v]);
             if (sizeof(A) == 4)  // (row minimum, item): lexicographic over the lane's rows
                 bkey = min(bkey, min(pack64(r0, i0), pack64(r1, i1)));
         }
@@ -982,10 +955,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         __syncwarp(FULL);
         {
             const uint32_t nb = p0 < nB ? min(cap, nB - p0) : 0u;
-            if (gath)
-                for (uint32_t u = gl; u < nb; u += GL) lp8[u] = T.el(__ldcg(gsp + p0 + u));
-            else
-                for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + p0 + u);
+            for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + p0 + u);
         }
         __syncwarp(FULL);
         }
@@ -1006,14 +976,10 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                     const A se = Bs.a - a.a, sl = Bs.b - a.b, pe = Bp.a + a.a, pl = Bp.b + a.b;
                     if (gl == 0 && (uint32_t)maxa(maxa(se, sl), maxa(pe, pl)) == S) rv = 0xFFFFFFFFull;
                     for (uint32_t v = gl; v < nB; v += GL) {
-                        const bool sm = v < cap && one_chunk;
-                        const uint32_t pj = (sm && gath) ? 0u : (sm ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v));
-                        const Pair2<A> b = (sm && gath) ? lp8[v] : T.el(pj);
+                        const uint32_t pj = (v < cap && one_chunk) ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v);
+                        const Pair2<A> b = T.el(pj);
                         const A sc = maxa(maxa<A>(se + b.a, sl + b.b), maxa<A>(pe - b.a, pl - b.b));
-                        if ((uint32_t)sc == S) {
-                            const uint32_t rk = T.idx((sm && gath) ? (uint32_t)__ldcg(gsp + v) : pj) + 1u;
-                            rv = min(rv, ((u64)rk << 32) | v);
-                        }
+                        if ((uint32_t)sc == S) rv = min(rv, ((u64)(T.idx(pj) + 1u) << 32) | v);
                     }
                 }
 #pragma unroll
@@ -1056,21 +1022,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             } else {
                 dirty = true;
             }
-            if (gl == 0 && gath) {  // FL is formed after the refinement
-                const Pair2<A> a = T.el(pi);
-                Pair2<A> es = EL[js], ep = EL[jp];
-                es.a -= a.a; es.b -= a.b;
-                ep.a += a.a; ep.b += a.b;
-                set_apos(apos, pi, jp, wide);
-                if (brk != 0u) {
-                    const Pair2<A> b = T.el(pj);
-                    ep.a -= b.a; ep.b -= b.b;
-                    es.a += b.a; es.b += b.b;
-                    set_apos(apos, pj, js, wide);
-                }
-                EL[js] = es;
-                EL[jp] = ep;
-            } else if (gl == 0) {
+            if (gl == 0) {
                 const ItemRec<A> a = T.item(pi);
                 const A ae = a.e, al = a.l;
                 Pair2<A> es = EL[js], fs = FL[js], ep = EL[jp], fp = FL[jp];
@@ -1286,23 +1238,17 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
         // split pipeline: k_lpt left this candidate's packed bucket keys (offset removed) and
         // its assignment; the caller copied the assignment into apos
         const uint2* src = reinterpret_cast<const uint2*>(p.lpt_el) + (size_t)ent * m;  // k_lpt's entry
-        constexpr bool gath = MODE == 2;  // FL shares the scratch: formed after the refinement
         for (uint32_t j = gl; j < m; j += GL) {
             const uint2 v = __ldcg(src + j);
             EL[j] = Pair2<A>{(A)v.x, (A)v.y};
-            if (!gath) FL[j] = Pair2<A>{0, 0};
+            FL[j] = Pair2<A>{0, 0};
         }
         __syncwarp(FULL);
         ph.mark(0);
         if (m >= 2 && p.R > 0)
-            refine<A, PK, GL, SM, gath, true>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
-        if (gath || !(m >= 2 && p.R > 0)) {
-            if (gath) {
-                for (uint32_t j = gl; j < m; j += GL) FL[j] = Pair2<A>{0, 0};
-                __syncwarp(FULL);
-            }
+            refine<A, PK, GL, SM, true>(p, T, c, sh, EL, FL, apos, scr, csr, gl, c >= 2, ph);
+        else
             form_fl<A, GL, SM>(p, T, apos, p.wide != 0, FL, gl);
-        }
     } else {
     for (uint32_t j = gl; j < m; j += GL) {
         // co: the LPT probe offset; the plain variant's lane-local LPT keys carry k = j / GL
@@ -1360,7 +1306,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
 }
 
 // MODE 0: the whole candidate (LPT, refinement, 1F1B); 1: the split pipeline's second kernel
-// (from k_lpt's output: refinement + 1F1B; packed u32 only); 2: the same in gather mode
+// (from k_lpt's output: refinement + 1F1B; packed u32 only)
 template <typename A, bool PK, int GL, bool SM, bool O4, int MODE = 0>
 __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
     if (p.hdr->variant != p.want_variant) return;  // another variant runs
@@ -1548,222 +1494,6 @@ __global__ void __launch_bounds__(kLptMaxThreads) k_lpt(CandParams p) {
     }
 }
 
-// ---------------------------------------------------------------- fused pipeline: one kernel
-// The split pipeline's two stages in one persistent kernel.  CTA b owns
-// the candidates [c_begin + b*Q, c_begin + (b+1)*Q) and a ring of f.ring global entries
-// (assignment + packed bucket keys).  Every warp owns f.region bytes of shared memory and
-// repeatedly takes either an LPT task (16 consecutive candidates, 2 lanes each, as k_lpt) or
-// a refinement task (RG = 32 / GLR consecutive candidates whose LPT is done: refinement and
-// 1F1B from the entry, as the split candidate kernel), so the SM's warps mix the ALU-bound
-// LPT with the latency- and shared-memory-bound refinement.  Scheduling state lives in shared
-// memory: the two claim counters, the number of warps refining, and per ring entry done[e] =
-// c + 1 (LPT of c written; the writer fences at GPU scope first, the entry is read from L2)
-// and used[e] = c + 1 (consumed).  A task is claimed with atomicCAS only once it is ready,
-// so no warp ever waits on a claimed task and the kernel cannot deadlock; a warp with
-// nothing to do sleeps briefly and gives up with DFLOP_DEV_PIPELINE_ERROR after
-// f.spin_limit empty polls (a safety net, never expected).  Policy: refine when a task is
-// ready and fewer than f.ref_warps warps refine (or no LPT task can start), else LPT.
-template <int GLR, bool O4>
-__global__ void __launch_bounds__(kFusedMaxThreads) k_fused(CandParams p, FusedParams f) {
-    if (p.hdr->variant != 0) return;  // the packed variant only
-    const uint32_t sh = p.hdr->shift, co = p.hdr->offs;
-    extern __shared__ __align__(128) uint8_t smem[];
-    const uint32_t nw = blockDim.x >> 5;
-    uint32_t* sched = reinterpret_cast<uint32_t*>(smem + p.tbl_bytes + (size_t)nw * f.region);
-    volatile uint32_t* vs = sched;  // [0] next LPT, [1] next refinement, [2] warps refining
-    volatile uint32_t* done = sched + 4;
-    volatile uint32_t* used = sched + 4 + f.ring;
-    const uint32_t Q = (p.c_end - p.c_begin + gridDim.x - 1) / gridDim.x;
-    const uint32_t cb = min(p.c_end, p.c_begin + blockIdx.x * Q), ce = min(p.c_end, cb + Q);
-    Tbl<uint32_t, true> T;
-    {
-        const uint32_t words = p.n * (uint32_t)sizeof(ItemRec<uint32_t>) / 16;
-        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
-            reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.items) + i);
-        uint16_t* pi16 = reinterpret_cast<uint16_t*>(smem + (size_t)p.n * sizeof(ItemRec<uint32_t>));
-        for (uint32_t i = threadIdx.x; i < p.n; i += blockDim.x) pi16[i] = (uint16_t)__ldg(p.pos_item + i);
-        for (uint32_t i = threadIdx.x; i < 4 + 2 * f.ring; i += blockDim.x) sched[i] = i < 2 ? cb : 0u;
-        __syncthreads();
-        T.it = reinterpret_cast<const ItemRec<uint32_t>*>(smem);
-        T.it_s = (uint32_t)__cvta_generic_to_shared(smem);
-        T.pi16 = pi16;
-        T.pi32 = nullptr;
-    }
-    bool forced = false;  // as in k_candidates
-    if (p.m >= 1 && p.m <= p.n) {
-        bool ok = true;
-        for (uint32_t q = threadIdx.x & 31u; q < p.m; q += 32) {
-            const Pair2<uint32_t> r = T.el(q);
-            ok = ok && r.a != 0 && r.b != 0;
-        }
-        forced = __all_sync(FULL, ok);
-    }
-    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5, m = p.m;
-    uint8_t* region = smem + p.tbl_bytes + (size_t)w * f.region;
-    // this CTA's ring: entries e + blockIdx.x * (ring + 1), the last one scratch
-    const size_t ring0 = (size_t)blockIdx.x * (f.ring + 1);
-    // refinement role: RG groups of GLR lanes, one persistent slot each
-    constexpr uint32_t RG = 32u / GLR;
-    const uint32_t rg = lane / GLR, rgl = lane % GLR;
-    const uint32_t slot = (blockIdx.x * nw + w) * RG + rg;
-    uint8_t* bufs = p.slot_apos + (size_t)slot * 2 * p.apos_bytes;
-    uint16_t* csr = p.slot_csr + (size_t)slot * p.csr_len;
-    for (uint32_t b = p.n + rgl; b < p.apos_bytes; b += GLR) {  // padding past n: never a bucket
-        bufs[b] = 0xFF;
-        bufs[p.apos_bytes + b] = 0xFF;
-    }
-    __syncwarp(FULL);
-    u64 best_key = p.slot_key[slot], best_T = 0, best_cmax = 0;
-    uint32_t best_buf = 0;
-    if (best_key != ~0ull) {
-        best_T = p.slot_T[slot];
-        best_cmax = p.slot_cmax[slot];
-        best_buf = p.slot_buf[slot];
-    }
-    uint32_t cur = best_buf ^ 1u;
-    // LPT role: 16 groups of 2 lanes
-    const uint32_t lg = lane >> 1, lgl = lane & 1u;
-    PhaseTimer ph;
-    ph.start(nullptr);
-    uint32_t idle = 0;
-    for (;;) {
-        uint32_t task = 0, arg = 0;  // 1: refinement of [arg, arg + RG), 2: LPT of [arg, arg + 16), 3: exit
-        if (lane == 0) {
-            const uint32_t r = vs[1], l = vs[0];
-            bool ready = r < ce;
-            const uint32_t re = min(r + RG, ce);
-            for (uint32_t c = r; c < re && ready; ++c) ready = done[(c - cb) % f.ring] == c + 1;
-            const uint32_t le = min(l + 16u, ce);
-            bool lpt_ok = l < ce;  // the ring entries' previous candidates are consumed
-            for (uint32_t c = l; c < le && lpt_ok; ++c)
-                if (c - cb >= f.ring) lpt_ok = used[(c - cb) % f.ring] == c - f.ring + 1;
-            if (f.roles) {  // fixed roles by scheduler: SMSPs 0, 1 run the LPT, 2, 3 refine
-                if ((w & 3u) < 2u)
-                    ready = false;
-                else
-                    lpt_ok = false;
-            }
-            const bool ref_first = ready && (vs[2] < f.ref_warps || !lpt_ok);
-            if (ref_first && atomicCAS(sched + 1, r, re) == r) {
-                task = 1;
-                arg = r;
-            } else if (lpt_ok && atomicCAS(sched, l, le) == l) {
-                task = 2;
-                arg = l;
-            } else if (ready && atomicCAS(sched + 1, r, re) == r) {
-                task = 1;
-                arg = r;
-            } else if (r >= ce && l >= ce) {
-                task = 3;
-            }
-            if (task == 1) atomicAdd(sched + 2, 1u);
-            if (task == 0 && ++idle > f.spin_limit) {
-                atomicOr(&p.hdr->status, (uint32_t)DFLOP_DEV_PIPELINE_ERROR);
-                task = 3;
-            }
-        }
-        task = __shfl_sync(FULL, task, 0);
-        arg = __shfl_sync(FULL, arg, 0);
-        __syncwarp(FULL);
-        if (task == 3) break;
-        if (task == 0) {
-            __nanosleep(64);
-            continue;
-        }
-        idle = 0;
-        if (task == 2) {
-            const uint32_t cc = arg + lg;
-            const bool valid = cc < arg + 16u && cc < ce;
-            const uint32_t c = valid ? cc : ce - 1;                     // tail groups recompute a real candidate
-            const uint32_t e = valid ? (cc - cb) % f.ring : f.ring;     // ... into the scratch entry
-            Pair2<uint32_t>* EL = reinterpret_cast<Pair2<uint32_t>*>(region + (size_t)lg * f.lpt_cb);
-            uint8_t* stage = region + (size_t)lg * f.lpt_cb + f.lpt_off_stage;
-            uint8_t* apos = p.lpt_apos + (ring0 + e) * p.apos_bytes;
-            for (uint32_t j = lgl; j < m; j += 2) EL[j] = Pair2<uint32_t>{j, j + co};
-            for (uint32_t b = p.n + lgl; b < p.apos_bytes; b += 2) apos[b] = 0xFF;
-            __syncwarp(FULL);
-            lpt_pass<uint32_t, true, 2, true>(p, T, c, sh, EL, EL, apos, stage, lgl, co, forced);
-            Pair2<uint32_t>* dst = reinterpret_cast<Pair2<uint32_t>*>(p.lpt_el) + (ring0 + e) * m;
-            for (uint32_t j = lgl; j < m; j += 2) {
-                const Pair2<uint32_t> x = EL[j];
-                __stcg(reinterpret_cast<unsigned long long*>(dst + j), pack64(x.b - co, x.a));
-            }
-            __threadfence();  // the entry reaches L2 before its flag
-            __syncwarp(FULL);
-            if (lgl == 0 && valid) done[e] = c + 1;
-        } else {
-            const uint32_t cc = arg + rg;
-            const bool valid = cc < ce;
-            const uint32_t c = valid ? cc : ce - 1;
-            const uint32_t e = (c - cb) % f.ring;
-            uint8_t* base = region + (size_t)rg * p.cand_bytes;
-            Pair2<uint32_t>* EL = reinterpret_cast<Pair2<uint32_t>*>(base);
-            Pair2<uint32_t>* FL = reinterpret_cast<Pair2<uint32_t>*>(base + p.off_fl);
-            uint8_t* scr = base + p.off_scr;
-            uint8_t* apos = bufs + (size_t)cur * p.apos_bytes;  // never the best buffer
-            {
-                const uint4* src = reinterpret_cast<const uint4*>(p.lpt_apos + (ring0 + e) * p.apos_bytes);
-                uint4* dst = reinterpret_cast<uint4*>(apos);
-                for (uint32_t b = rgl; b < p.apos_bytes / 16; b += GLR) dst[b] = __ldcg(src + b);
-                __syncwarp(FULL);
-            }
-            u64 Tc, cmax;
-            run_candidate<uint32_t, true, GLR, true, O4, 1>(p, T, c, sh, co, EL, FL, apos, scr, csr, rgl, Tc, cmax,
-                                                             ph, forced, (uint32_t)(ring0 + e));
-            __syncwarp(FULL);
-            if (rgl == 0 && valid) used[e] = c + 1;  // the entry may be reused
-            if (lane == 0) atomicSub(sched + 2, 1u);
-            Tc = __shfl_sync(FULL, Tc, 0, GLR);
-            u64 key;
-            if (Tc >= (1ull << 40)) {
-                if (rgl == 0) atomicOr(&p.hdr->status, (uint32_t)DFLOP_DEV_MAKESPAN_OVERFLOW);
-                key = (((1ull << 40) - 1) << 24) | (u64)(p.id_base + c);
-            } else {
-                key = (Tc << 24) | (u64)(p.id_base + c);
-            }
-            if (valid) {
-                if (rgl == 0 && p.cand_T) {
-                    p.cand_T[c - p.c_begin] = Tc;
-                    p.cand_cmax[c - p.c_begin] = cmax;
-                }
-                if (key < best_key) {
-                    best_key = key;
-                    best_T = Tc;
-                    best_cmax = cmax;
-                    best_buf = cur;
-                    cur ^= 1u;
-                }
-            }
-        }
-    }
-    if (rgl == 0) {
-        p.slot_key[slot] = best_key;
-        p.slot_T[slot] = best_T;
-        p.slot_cmax[slot] = best_cmax;
-        p.slot_buf[slot] = best_buf;
-        if (best_key != ~0ull) atomicMin(&p.hdr->best_key, best_key);
-    }
-}
-
-template <bool O4>
-static const void* ptr_fused_gl(int gl) {
-    switch (gl) {
-        case 8: return reinterpret_cast<const void*>(&k_fused<8, O4>);
-        case 16: return reinterpret_cast<const void*>(&k_fused<16, O4>);
-        default: return reinterpret_cast<const void*>(&k_fused<32, O4>);
-    }
-}
-
-template <bool O4>
-static void launch_fused_gl(int gl, uint32_t grid, uint32_t threads, size_t dyn, const CandParams& p,
-                            const FusedParams& f, cudaStream_t s) {
-    switch (gl) {
-        case 8: k_fused<8, O4><<<grid, threads, dyn, s>>>(p, f); break;
-        case 16: k_fused<16, O4><<<grid, threads, dyn, s>>>(p, f); break;
-        default: k_fused<32, O4><<<grid, threads, dyn, s>>>(p, f); break;
-    }
-}
-
 template <typename A, bool PK, bool SM, bool O4>
 static const void* ptr_gl(int gl) {
     switch (gl) {
@@ -1809,15 +1539,10 @@ static void launch_split_gl(const CandLaunch& L, const CandParams& p, cudaStream
     }
 }
 
-#define DFLOP_SPLIT_UNIT(NAME, O4)                                                               \
-    const void* split_ptr_##NAME(int mode, int gl) {                                              \
-        return mode == 2 ? ptr_split_gl<O4, 2>(gl) : ptr_split_gl<O4, 1>(gl);                     \
-    }                                                                                             \
-    void split_launch_##NAME(int mode, const CandLaunch& L, const CandParams& p, cudaStream_t s) { \
-        if (mode == 2)                                                                            \
-            launch_split_gl<O4, 2>(L, p, s);                                                      \
-        else                                                                                      \
-            launch_split_gl<O4, 1>(L, p, s);                                                      \
+#define DFLOP_SPLIT_UNIT(NAME, O4)                                                   \
+    const void* split_ptr_##NAME(int gl) { return ptr_split_gl<O4, 1>(gl); }          \
+    void split_launch_##NAME(const CandLaunch& L, const CandParams& p, cudaStream_t s) { \
+        launch_split_gl<O4, 1>(L, p, s);                                              \
     }
 
 // one translation unit per (variant, table placement, ORDER4) so the 72 instantiations build

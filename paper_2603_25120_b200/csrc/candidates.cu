@@ -28,20 +28,18 @@ void cand_launch_v2g(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 const void* cand_ptr_v2g_o4(int gl);
 void cand_launch_v2g_o4(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 
-const void* split_ptr_plain(int mode, int gl);
-void split_launch_plain(int mode, const CandLaunch& L, const CandParams& p, cudaStream_t s);
-const void* split_ptr_o4(int mode, int gl);
-void split_launch_o4(int mode, const CandLaunch& L, const CandParams& p, cudaStream_t s);
+const void* split_ptr_plain(int gl);
+void split_launch_plain(const CandLaunch& L, const CandParams& p, cudaStream_t s);
+const void* split_ptr_o4(int gl);
+void split_launch_o4(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 
-const void* split_kernel_ptr(int mode, int gl, bool o4) {
-    return o4 ? split_ptr_o4(mode, gl) : split_ptr_plain(mode, gl);
-}
+const void* split_kernel_ptr(int gl, bool o4) { return o4 ? split_ptr_o4(gl) : split_ptr_plain(gl); }
 
-void split_launch(int mode, const CandLaunch& L, const CandParams& p, cudaStream_t s) {
+void split_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s) {
     if (p.order4)
-        split_launch_o4(mode, L, p, s);
+        split_launch_o4(L, p, s);
     else
-        split_launch_plain(mode, L, p, s);
+        split_launch_plain(L, p, s);
 }
 
 const void* cand_kernel_ptr(int variant, int gl, bool tbl_smem, bool o4) {

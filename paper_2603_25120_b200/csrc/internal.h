@@ -90,10 +90,7 @@ struct BalanceConfig {
     // split pipeline (packed variant only): k_lpt with lpt_gl lanes per candidate, then the
     // candidate kernel on its output, over chunks of lpt_chunk candidates
     bool split = false;
-    bool gather = false;               // CandParams::gather for the split candidate kernel
-    // fused pipeline (k_fused): warps per CTA, shared-memory bytes per warp, ring entries
-    bool fused = false;
-    uint32_t fz_warps = 0, fz_region = 0, fz_ring = 0, fz_lcb = 0;
+
     int lpt_gl = 0;
     uint32_t lpt_cpb = 0, lpt_grid = 0, lpt_tbl = 0, lpt_cb = 0, lpt_chunk = 0;
     // workspace layout (byte offsets)

@@ -190,16 +190,10 @@ def test_balance_shard_window_config5(D, O, presets):
     (2500, 250, 1, 5000),     # m = 250: GL = 4, generic
     (40, 64, 1, 2 ** 20),     # n < m
 ])
-@pytest.mark.parametrize("pipe", ["chunked", "gather", "fused", "fused_ring64"])
-def test_split_pipeline_parity(D, O, presets, monkeypatch, n, n_mb, l_dp, hi, pipe):
-    """The split pipeline (the LPT in k_lpt, then the candidate kernel from its output -- chunk
-    by chunk, or both in the persistent k_fused through a ring, here also a 64-entry ring that
-    wraps many times) forced on (DFLOP_SPLIT=2): every candidate equals
-    the merged kernel's (DFLOP_SPLIT=0) and, on a window, the oracle's."""
-    monkeypatch.setenv("DFLOP_SPLIT_GATHER", "1" if pipe == "gather" else "0")
-    monkeypatch.setenv("DFLOP_FUSED", "1" if pipe.startswith("fused") else "0")
-    if pipe == "fused_ring64":
-        monkeypatch.setenv("DFLOP_FUSED_RING", "64")
+def test_split_pipeline_parity(D, O, presets, monkeypatch, n, n_mb, l_dp, hi):
+    """The split pipeline (the LPT in k_lpt, then the candidate kernel from its output, chunk by
+    chunk) forced on (DFLOP_SPLIT=2): every candidate equals the merged
+    kernel's (DFLOP_SPLIT=0) and, on a window, the oracle's."""
     p = presets[5]
     if hi is None:
         q = O.predict(p.model, p.plan, *p.features(1))[1]
