@@ -883,6 +883,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         A bsc = amax<A>();
         uint32_t bi = 0xFFFFFFFFu, brk = 0xFFFFFFFFu, vstar = 0xFFFFFFFFu;
         u64 bkey = ~0ull;  // 32-bit scores: (row minimum << 32 | item), branch-free minima
+        uint32_t ubest = 0;  // ... and the j* list index of the lane's best row
         // all (i, i') with i in j*, i' in {NONE} u j'; lexicographic min of (score, i, rank(i'))
         // two j* members per lane and step: every j' member loaded once serves two pairs
         auto ival = [&](uint32_t u, uint32_t& ii, A& se, A& sl, A& pe, A& pl) {
@@ -947,8 +948,17 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 pair(q3);
             }
             for (; v < nBs; ++v) pair(lp[v]);
-            if (sizeof(A) == 4)  // (row minimum, item): lexicographic over the lane's rows
-                bkey = min(bkey, min(pack64(r0, i0), pack64(r1, i1)));
+            if (sizeof(A) == 4) {  // (row minimum, item): lexicographic over the lane's rows
+                const u64 k0 = pack64(r0, i0), k1 = pack64(r1, i1);
+                if (k0 < bkey) {
+                    bkey = k0;
+                    ubest = u;
+                }
+                if (k1 < bkey) {  // (a duplicated first row ties, never below)
+                    bkey = k1;
+                    ubest = u + GL;
+                }
+            }
         }
         p0 += cap;
         if (!__any_sync(FULL, p0 < nB)) break;  // warp-uniform
@@ -960,9 +970,17 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         __syncwarp(FULL);
         }
         ph.mark(3);
+        uint32_t ustar = 0, pistar = 0;  // the winning row: j* list index and position (32-bit)
         if (sizeof(A) == 4) {
+            const u64 mine = bkey;
 #pragma unroll
             for (int off = GL / 2; off > 0; off >>= 1) bkey = min(bkey, __shfl_xor_sync(FULL, bkey, off));
+            {  // the lane holding the winning row (keys are unique: one lane) broadcasts its index
+                const uint32_t gbase = (threadIdx.x & 31u) & ~(uint32_t)(GL - 1);
+                const uint32_t bal = __ballot_sync(FULL, mine == bkey);
+                const uint32_t gm = GL == 32 ? bal : (bal >> gbase) & ((1u << (GL & 31)) - 1u);
+                ustar = __shfl_sync(FULL, ubest, gbase + (gm ? (uint32_t)(__ffs(gm) - 1) : 0u));
+            }
             // phase 2 (only when the move would be applied): the least rank among the partners
             // of the winning row that reach the minimum -- the same lexicographic minimum
             // (score, i, rank) as one pass over 64-bit keys
@@ -972,7 +990,8 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                 // (rank << 32 | list index v): the apply step edits entry v of j''s list directly
                 u64 rv = ~0ull;
                 if (need) {
-                    const Pair2<A> a = T.el(__ldg(p.item_pos + istar));
+                    pistar = ustar < cap ? (uint32_t)ls[ustar] : (uint32_t)__ldcg(gss + ustar);
+                    const Pair2<A> a = T.el(pistar);
                     const A se = Bs.a - a.a, sl = Bs.b - a.b, pe = Bp.a + a.a, pl = Bp.b + a.b;
                     if (gl == 0 && (uint32_t)maxa(maxa(se, sl), maxa(pe, pl)) == S) rv = 0xFFFFFFFFull;
                     for (uint32_t v = gl; v < nB; v += GL) {
@@ -995,11 +1014,31 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             lexmin_reduce<A, GL>(bsc, bi, brk, FULL);
         }
         if (apply && bi != 0xFFFFFFFFu && bsc < Ws) {  // uniform in the group (reduced values)
-            const uint32_t pi = __ldg(p.item_pos + bi);
-            const uint32_t pj = brk != 0u ? __ldg(p.item_pos + (brk - 1u)) : 0xFFFFFFFFu;
+            // 32-bit: the winning row and partner are known by their list indices (ustar, vstar)
+            uint32_t pi, pj;
+            if (sizeof(A) == 4) {
+                pi = pistar;
+                pj = brk != 0u ? ((vstar < cap && one_chunk) ? (uint32_t)lp[vstar] : (uint32_t)__ldcg(gsp + vstar))
+                               : 0xFFFFFFFFu;
+            } else {
+                pi = __ldg(p.item_pos + bi);
+                pj = brk != 0u ? __ldg(p.item_pos + (brk - 1u)) : 0xFFFFFFFFu;
+            }
             // a move adds a member to j': it needs a free entry, else the lists are rebuilt
             const bool fits = brk != 0u || nB < off[jp + 1] - off[jp];
-            if (fits) {  // i leaves j*'s list (replaced by i', or by the last member)
+            if (fits && sizeof(A) == 4) {  // i leaves j*'s list (replaced by i', or by the last member)
+                if (gl == 0) {
+                    const uint32_t last = nA - 1u < cap ? (uint32_t)ls[nA - 1u] : (uint32_t)__ldcg(gss + nA - 1u);
+                    gss[ustar] = (uint16_t)(brk != 0u ? pj : last);
+                    if (brk != 0u) {  // i' leaves j''s list (entry vstar), i takes it
+                        gsp[vstar] = (uint16_t)pi;
+                    } else {
+                        gsp[nB] = (uint16_t)pi;
+                        cnt[js] = nA - 1u;
+                        cnt[jp] = nB + 1u;
+                    }
+                }
+            } else if (fits) {
                 for (uint32_t u = gl; u < nA; u += GL) {
                     const uint32_t q = u < cap ? (uint32_t)ls[u] : (uint32_t)__ldcg(gss + u);
                     if (q == pi) {
@@ -1007,9 +1046,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
                         gss[u] = (uint16_t)(brk != 0u ? pj : last);
                     }
                 }
-                if (brk != 0u && sizeof(A) == 4) {  // i' leaves j''s list (entry vstar), i takes it
-                    if (gl == 0) gsp[vstar] = (uint16_t)pi;
-                } else if (brk != 0u) {
+                if (brk != 0u) {
                     for (uint32_t v = gl; v < nB; v += GL) {
                         const uint32_t q = (v < cap && one_chunk) ? (uint32_t)lp[v] : (uint32_t)__ldcg(gsp + v);
                         if (q == pj) gsp[v] = (uint16_t)pi;
