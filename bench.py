@@ -431,7 +431,9 @@ def main():
         peak_alu = peak_issue / 2
         note = "fallback: 148 SM x 4 SMSP x 32 lanes x 1965 MHz (profiles/int_peaks.json missing)"
     variant = "u64" if wide_sums else "u32"
-    kname = f"k_candidates<{variant}>" if variant == "u64" else "k_lpt + k_candidates<u32> (split pipeline)"
+    kname = f"k_candidates<{variant}>"
+    if variant == "u32" and prof.get("split_chunks"):  # the host launched the split pipeline
+        kname = "k_lpt + k_candidates<u32> (split pipeline, %d chunks per step)" % (prof["split_chunks"] // args.steps)
     roofline = {"bound": "issue", "kernel": kname, "achieved": achieved, "peak": peak_issue,
                 "unit": "Tops/s", "frac": achieved / peak_issue, "traffic": None,
                 "peak_alu_pipe": peak_alu, "frac_alu_pipe": achieved / peak_alu,
@@ -459,7 +461,7 @@ def main():
                                                      "Newton sequence of ~10 fp64 instructions")
         roofline["duration_note"] = "device step time (Stage A + Stage B)"
     # traffic: dram__bytes_read.sum + dram__bytes_write.sum of the candidate kernel from the
-    # committed ncu --set full capture (profiles/traffic.json), per candidate x this launch's K
+    # committed ncu capture (profiles/traffic.json), per candidate x this launch's K
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         tr = json.load(open(traffic_file)).get(p.name)
@@ -471,8 +473,7 @@ def main():
             # the issue roofline the kernel runs at, beside the algorithmic-op fraction above
             if "ncu_issue_active" in tr:
                 roofline["ncu_issue_active"] = tr["ncu_issue_active"]
-                roofline["ncu_threads_per_warp_instruction"] = tr.get("ncu_threads_per_warp_instruction")
-                for k in ("ncu_lsu_data_pipe_wavefronts", "ncu_alu_pipe"):  # the two busiest pipes
+                for k in ("ncu_lsu_data_pipe_wavefronts", "ncu_alu_pipe", "ncu_per_kernel"):  # the busiest pipes
                     if k in tr:
                         roofline[k] = tr[k]
 

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DFLOP_ABI_VERSION 4u
+#define DFLOP_ABI_VERSION 5u
 
 typedef int32_t dflop_status;
 #define DFLOP_OK 0
@@ -235,7 +235,8 @@ typedef struct dflop_profile {
     uint64_t kernel_launches; /* all libdflop kernel launches since the last reset    */
     double cand_ms;           /* summed device time of the timed candidate launches   */
     uint32_t stage_a_launches; /* Stage-A kernel launches timed (ALG1 searches)        */
-    uint32_t reserved;
+    uint32_t split_chunks;     /* candidate chunks run by the split pipeline (k_lpt, then the
+                                  candidate kernel) since the last reset */
     double stage_a_ms;        /* their summed device time                            */
 } dflop_profile;
 dflop_status dflop_profile_enable(int on);

@@ -689,6 +689,7 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
                 lpt_launch(cfg.lpt_gl, cfg.lpt_grid, cfg.lpt_cpb, ldyn, ql, s);
                 split_launch(L, q, s);
                 launches += 2;
+                count_split_chunks(1);
             }
             launches -= 1;
         } else {

@@ -29,6 +29,7 @@ int prof_begin(cudaStream_t s);
 void prof_mark(int idx, int which, cudaStream_t s);  // which: 1 = between variants, 2 = end
 // Stage-A kernel timing (dflop_profile.stage_a_ms): begin returns a mark index or -1
 int prof_stage_begin(cudaStream_t s);
+void count_split_chunks(uint32_t k);
 void prof_stage_end(int idx, cudaStream_t s);
 dflop_status cuda_status(cudaError_t e, const char* what);
 

@@ -11,6 +11,7 @@ namespace dflop {
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint32_t> g_split{0};
 std::atomic<bool> g_on{false};
 std::mutex g_mu;
 struct Mark {
@@ -22,6 +23,7 @@ std::vector<Mark> g_stage;   // Stage-A kernel marks (e[0], e[1])
 }  // namespace
 
 void count_launches(uint32_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+void count_split_chunks(uint32_t k) { g_split.fetch_add(k, std::memory_order_relaxed); }
 bool profiling() { return g_on.load(std::memory_order_relaxed); }
 
 int prof_begin(cudaStream_t s) {
@@ -123,8 +125,9 @@ extern "C" dflop_status dflop_profile_read(dflop_profile* out, int reset) {
     out->kernel_launches = g_launches.load();
     out->cand_ms = ms;
     out->stage_a_launches = (uint32_t)g_stage.size();
-    out->reserved = 0;
+    out->split_chunks = g_split.load();
     out->stage_a_ms = sms;
+    if (reset) g_split.store(0);
     if (reset) {
         for (auto& m : g_marks) g_free.push_back(m);
         for (auto& m : g_stage) g_free.push_back(m);

@@ -115,7 +115,7 @@ class PlanResult(C.Structure):
 
 class Profile(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("cand_launches", C.c_uint32), ("kernel_launches", C.c_uint64),
-                ("cand_ms", C.c_double), ("stage_a_launches", C.c_uint32), ("reserved", C.c_uint32),
+                ("cand_ms", C.c_double), ("stage_a_launches", C.c_uint32), ("split_chunks", C.c_uint32),
                 ("stage_a_ms", C.c_double)]
 
 
@@ -300,7 +300,8 @@ def profile_read(reset: bool = True) -> Dict:
     pr.struct_size = C.sizeof(Profile)
     _check(lib().dflop_profile_read(C.byref(pr), 1 if reset else 0))
     return dict(cand_launches=pr.cand_launches, kernel_launches=pr.kernel_launches, cand_ms=pr.cand_ms,
-                stage_a_launches=pr.stage_a_launches, stage_a_ms=pr.stage_a_ms)
+                stage_a_launches=pr.stage_a_launches, stage_a_ms=pr.stage_a_ms,
+                split_chunks=pr.split_chunks)
 
 
 def predict_costs(model: Dict, plan: Dict, tiles, frames, text, want_f32: bool = True, dev_status=None, stream=None):

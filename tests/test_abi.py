@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(D):
 
 
 def test_abi_version_and_last_error(D):
-    assert D.abi_version() == 4
+    assert D.abi_version() == 5
     assert D.lib().dflop_last_error() == b""
 
 
