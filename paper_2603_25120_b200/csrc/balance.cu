@@ -428,7 +428,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     uint32_t lcpb = ltbl < smem_max ? (uint32_t)std::min<size_t>((smem_max - ltbl) / lcb, kLptMaxThreads / lg) : 0;
     lcpb = lcpb / lpw * lpw;
     const bool split_pre = sh.split_ok && split_env != 0 && !(sh.mode & DFLOP_MODE_EXHAUSTIVE) && m >= 48 &&
-                           !wide && n > 0 && gl >= 8 && lcpb >= 4 * lpw &&
+                           !wide && n > 0 && n <= 4096 && gl >= 8 && lcpb >= 4 * lpw &&
                            (sh.n_cand >= 2 * nsm * lcpb || split_env == 2);
     // the split candidate kernel runs no LPT: stagger its candidates for the refinement's
     // broadcast reads (4 candidates of a warp on distinct banks) instead of the probe loads
@@ -439,7 +439,9 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     };
     auto layout = [&](int v, uint32_t cap) {
         Lay L;
-        const uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cap, rings));
+        uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cap, rings));
+        if (v == 0 && split_pre)  // the split kernel: rows' copy, then 64 sorted partner keys
+            scr = round16(std::max(round16(8u * m + 4u + 2u * cap) + 256u, rings));
         const uint32_t asz = v == 2 ? 8u : 4u;
         const uint32_t el = round16(m * 2u * asz);   // EL[m] then FL[m]
         uint32_t cb = 2 * el + scr;

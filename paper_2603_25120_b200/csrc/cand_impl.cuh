@@ -800,6 +800,40 @@ DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, ui
     __syncwarp(FULL);
 }
 
+// Ascending bitonic sort of 64 keys held KPL = 64 / GL per lane by the GL lanes of a group
+// (element e = KPL * gl + t): in-register compare-exchanges below distance KPL, lane
+// exchanges (xor shuffles inside the group) above it.  All lanes of the warp take part.
+template <int GL, int KPL>
+DFLOP_DEV void bitonic_sort64(uint32_t (&key)[KPL], uint32_t gl) {
+#pragma unroll
+    for (uint32_t k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j < (uint32_t)KPL) {
+#pragma unroll
+                for (uint32_t t = 0; t < (uint32_t)KPL; ++t) {
+                    if ((t & j) == 0) {
+                        const bool asc = ((KPL * gl + t) & k) == 0;
+                        const uint32_t x = key[t], y = key[t ^ j];
+                        const uint32_t lo = min(x, y), hi = max(x, y);
+                        key[t] = asc ? lo : hi;
+                        key[t ^ j] = asc ? hi : lo;
+                    }
+                }
+            } else {
+                const uint32_t lx = j / KPL;
+                const bool lower = (gl & lx) == 0;
+#pragma unroll
+                for (uint32_t t = 0; t < (uint32_t)KPL; ++t) {
+                    const bool asc = ((KPL * gl + t) & k) == 0;
+                    const uint32_t o = __shfl_xor_sync(FULL, key[t], lx);
+                    key[t] = (lower == asc) ? min(key[t], o) : max(key[t], o);
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- swap refinement (O6)
 // `apply` is false for c < 2: the rounds are still executed (and discarded) so that every
 // group of a warp issues the same shuffle sequence.
@@ -825,6 +859,12 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
     }
     uint32_t* off = cnt + m;
     uint16_t* lp = ls + cap;
+    // SRT (split kernel, 32-bit sums, table in shared memory, n <= 4096): j''s members are
+    // sorted by their load in the narrower of the two dimensions and each row scans only the
+    // window of partners that could bring the pair below W* (DESIGN.md section 6); the sorted
+    // keys (load with the low 12 bits replaced by the position) follow the row copy
+    constexpr bool SRT = CS && SM && sizeof(A) == 4 && GL >= 8;
+    uint32_t* sk = reinterpret_cast<uint32_t*>(scr + ((4u * (2u * m + 1u) + 2u * cap + 15u) & ~15u));
     bool dirty = true;  // the lists must be (re)built from the assignment
     bool first = true;  // the first build also forms FL (LPT maintains EL only)
     for (uint32_t r = 0; r < p.R; ++r) {
@@ -876,7 +916,8 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         {
             const uint32_t na = min(nA, cap), nb = min(nB, cap);
             for (uint32_t u = gl; u < na; u += GL) ls[u] = __ldcg(gss + u);
-            for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + u);
+            if (!SRT)
+                for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + u);
         }
         __syncwarp(FULL);
         ph.mark(2);
@@ -898,7 +939,63 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
         // j''s members in chunks of cap: each chunk copied to shared memory (the first above)
         // and paired with every row; the row minima fold into bkey chunk by chunk (the NONE
         // pair in every chunk: idempotent)
-        const bool one_chunk = nB <= cap;  // phase 2 / apply may read the copy
+        const bool one_chunk = !SRT && nB <= cap;  // phase 2 / apply may read the copy
+        if constexpr (SRT) {
+            // A pair can bring j* below W* only if all four loads drop below it: x' in
+            // (pe - W*, W* - se) for the partner's e (x' = a) and (pl - W*, W* - sl) for its l --
+            // a window of width 2W* - E*(j*) - E*(j') (resp. L), the same for every row.  The
+            // other pairs cannot win (the move needs a score below W*), so each row scores only
+            // the partners inside its window of the narrower dimension (and the NONE pair).
+            constexpr uint32_t KPL = 64u / GL;
+            const u64 wE = (u64)(Ws - Bs.a) + (u64)(Ws - Bp.a), wL = (u64)(Ws - Bs.b) + (u64)(Ws - Bp.b);
+            const bool dimE = wE <= wL;
+            for (uint32_t p0 = 0;; p0 += 64) {  // chunks of 64 partners
+                const uint32_t nb = p0 < nB ? min(64u, nB - p0) : 0u;
+                uint32_t key[KPL];
+#pragma unroll
+                for (uint32_t t = 0; t < KPL; ++t) {
+                    const uint32_t v = KPL * gl + t;
+                    key[t] = 0xFFFFFFFFu;
+                    if (v < nb) {
+                        const uint32_t pos = __ldcg(gsp + p0 + v);
+                        const Pair2<A> b = T.el(pos);
+                        key[t] = ((uint32_t)(dimE ? b.a : b.b) & ~0xFFFu) | pos;
+                    }
+                }
+                bitonic_sort64<GL, KPL>(key, gl);
+#pragma unroll
+                for (uint32_t t = 0; t < KPL; ++t) sk[KPL * gl + t] = key[t];
+                __syncwarp(FULL);
+                for (uint32_t u = gl; u < nA && (p0 == 0 || nb > 0); u += GL) {
+                    const uint32_t pi = u < cap ? (uint32_t)ls[u] : (uint32_t)__ldcg(gss + u);
+                    const Pair2<A> a = T.el(pi);
+                    const uint32_t ii = T.idx(pi);
+                    const uint32_t se = (uint32_t)(Bs.a - a.a), sl = (uint32_t)(Bs.b - a.b);
+                    const uint32_t pe = (uint32_t)(Bp.a + a.a), pl = (uint32_t)(Bp.b + a.b);
+                    uint32_t rr = max(max(se, sl), max(pe, pl));  // NONE
+                    const uint32_t W = (uint32_t)Ws, lo_t = dimE ? pe : pl, hi_t = dimE ? se : sl;
+                    const uint32_t qlo = lo_t < W ? 0u : ((lo_t - W + 1u) & ~0xFFFu);  // x' > lo_t - W*
+                    const uint32_t hi = W - hi_t;                                       // x' < hi
+                    const uint32_t qhi = (hi - 1u) & ~0xFFFu;
+                    const uint32_t limit = hi == 0u ? 0u : (qhi >= 0xFFFFF000u ? 0xFFFFFFFFu : qhi + 0x1000u);
+                    uint32_t k = 0;
+#pragma unroll
+                    for (uint32_t st = 32; st > 0; st >>= 1)
+                        if (sk[k + st - 1] < qlo) k += st;
+                    for (; k < nb && sk[k] < limit; ++k) {
+                        const Pair2<A> b = T.el(sk[k] & 0xFFFu);
+                        rr = min(rr, score4(se, sl, pe, pl, (uint32_t)b.a, (uint32_t)b.b));
+                    }
+                    const u64 kk = pack64(rr, ii);
+                    if (kk < bkey) {
+                        bkey = kk;
+                        ubest = u;
+                    }
+                }
+                if (!__any_sync(FULL, p0 + 64 < nB)) break;  // warp-uniform
+                __syncwarp(FULL);
+            }
+        } else {
         for (uint32_t p0 = 0;;) {
         const uint32_t nBs = p0 < nB ? min(cap, nB - p0) : 0u;
         for (uint32_t u = gl; u < nA && (p0 == 0 || nBs > 0); u += 2 * GL) {
@@ -968,6 +1065,7 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
             for (uint32_t u = gl; u < nb; u += GL) lp[u] = __ldcg(gsp + p0 + u);
         }
         __syncwarp(FULL);
+        }
         }
         ph.mark(3);
         uint32_t ustar = 0, pistar = 0;  // the winning row: j* list index and position (32-bit)
