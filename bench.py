@@ -438,7 +438,10 @@ def main():
                 "unit": "Tops/s", "frac": achieved / peak_issue, "traffic": None,
                 "peak_alu_pipe": peak_alu, "frac_alu_pipe": achieved / peak_alu,
                 "kernel_ms": cand_ms, "kernel_share_of_step": cand_ms / ms_per_step,
-                "peak_note": note, "ops_per_candidate": ops_launch / max(1, (e - b) * P)}
+                "peak_note": note, "ops_per_candidate": ops_launch / max(1, (e - b) * P),
+                "ops_note": "nominal work of the method (DESIGN.md section 8); the split pipeline's windowed "
+                            "refinement search scores only the pairs that could be applied (about 2% on config 5) "
+                            "with the same result -- ncu_* give the executed-instruction utilisation"}
     stage_a = None
     if alg1:
         roofline["kernel"] = "k_candidates<u32> x P plans (Stage B, 4 streams)"
