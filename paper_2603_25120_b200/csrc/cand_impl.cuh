@@ -160,6 +160,39 @@ DFLOP_DEV uint64_t batch_perms(uint32_t g0, uint32_t W, uint32_t nc, uint32_t c,
                                uint32_t k1) {
     constexpr uint32_t cw = 32u / GL;  // candidate groups per warp
     const uint32_t lane = threadIdx.x & 31u;
+    if (cw * W == 32u) {
+        // one Fisher-Yates per lane: the lane draws its own group's Philox words (no exchange)
+        const uint32_t cg = lane / W, gg = lane % W;
+        const uint32_t cc = __shfl_sync(FULL, c, cg * GL);
+        const uint32_t start = (g0 + gg) * G;
+        const uint32_t ng = start < n ? min(G, n - start) : 0u;
+        uint64_t perm = 0xFEDCBA9876543210ull;
+        uint32_t p32 = 0x76543210u;
+        const bool narrow = G <= 8;
+        for (uint32_t pc = 0; pc < nc; ++pc) {
+            const Philox4 r = philox4x32_10(g0 + gg, cc, 0u, pc, k0, k1);
+            const uint32_t wq[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t idx = pc * 4 + q;
+                if (idx + 1 < ng) {
+                    const uint32_t tt = ng - 1 - idx;
+                    const uint32_t rr = mulhi32(wq[q], tt + 1);
+                    if (narrow) {
+                        const uint32_t x = ((p32 >> (4 * tt)) ^ (p32 >> (4 * rr))) & 15u;
+                        p32 ^= (x << (4 * tt)) | (x << (4 * rr));
+                    } else {
+                        const uint64_t a = (perm >> (4 * tt)) & 15ull, b = (perm >> (4 * rr)) & 15ull;
+                        const uint64_t x = a ^ b;
+                        perm ^= (x << (4 * tt)) | (x << (4 * rr));
+                    }
+                }
+            }
+        }
+        if (narrow) perm = 0xFEDCBA9800000000ull | p32;
+        if (cc < 2) perm = 0xFEDCBA9876543210ull;
+        return perm;
+    }
     const uint32_t per_cg = W * nc, tasks = cw * per_cg;
     uint32_t w[4][4];
 #pragma unroll
