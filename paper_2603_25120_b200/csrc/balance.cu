@@ -429,7 +429,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     lcpb = lcpb / lpw * lpw;
     const bool split_pre = sh.split_ok && split_env != 0 && !(sh.mode & DFLOP_MODE_EXHAUSTIVE) && m >= 48 &&
                            !wide && n > 0 && n <= 4096 && gl >= 8 && lcpb >= 4 * lpw &&
-                           (sh.n_cand >= 2 * nsm * lcpb || split_env == 2);
+                           (sh.n_cand >= 4096 || split_env == 2);
     // the split candidate kernel runs no LPT: stagger its candidates for the refinement's
     // broadcast reads (4 candidates of a warp on distinct banks) instead of the probe loads
     const int stg_env = env_int("DFLOP_SPLIT_STAGGER", 48);
