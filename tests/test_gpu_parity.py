@@ -189,17 +189,34 @@ def test_balance_shard_window_config5(D, O, presets):
     (1500, 64, 2, 2 ** 18),   # m = 128: GL = 4, 32 buckets per lane
     (2500, 250, 1, 5000),     # m = 250: GL = 4, generic
     (40, 64, 1, 2 ** 20),     # n < m
+    (4000, 50, 1, "ldom"),    # the LLM dimension is the bottleneck: windows on l
+    (4000, 50, 1, "many"),    # ~80 members per bucket: partner lists sorted in two chunks
+    (3000, 48, 1, "ties"),    # three cost values: exact ties on and at the window edges
+    (3000, 64, 1, "quant"),   # loads that differ below the keys' 12-bit quantisation
 ])
 def test_split_pipeline_parity(D, O, presets, monkeypatch, n, n_mb, l_dp, hi):
     """The split pipeline (the LPT in k_lpt, then the candidate kernel from its output, chunk by
     chunk) forced on (DFLOP_SPLIT=2): every candidate equals the merged
     kernel's (DFLOP_SPLIT=0) and, on a window, the oracle's."""
     p = presets[5]
+    rng = np.random.default_rng(n + n_mb)
     if hi is None:
         q = O.predict(p.model, p.plan, *p.features(1))[1]
         plan = p.plan
+    elif isinstance(hi, str):
+        if hi == "ldom":
+            q = np.stack([rng.integers(0, 3000, n), rng.integers(0, 3000, n),
+                          rng.integers(0, 60000, n), rng.integers(0, 60000, n)])
+        elif hi == "many":
+            q = rng.integers(0, 400, (4, n))
+            q[:, rng.random(n) < 0.02] *= 300  # a few large samples
+        elif hi == "ties":
+            q = rng.choice(np.array([0, 1000, 3000]), size=(4, n))
+        else:  # "quant": 50,000 + a few ticks: the packed loads agree above the low 12 bits
+            q = 50_000 + rng.integers(0, 40, (4, n))
+        q = q.astype(np.uint32)
+        plan = dict(e_tp=1, e_pp=2, e_dp=1, l_tp=1, l_pp=6, l_dp=l_dp, n_mb=n_mb)
     else:
-        rng = np.random.default_rng(n + n_mb)
         q = rng.integers(0, hi, (4, n), dtype=np.uint64).astype(np.uint32)
         q[:, rng.random(n) < 0.2] = q[:, [0]]  # exact ties
         plan = dict(e_tp=1, e_pp=2, e_dp=1, l_tp=1, l_pp=6, l_dp=l_dp, n_mb=n_mb)
