@@ -595,3 +595,23 @@ def test_makespan_overflow_flag(D):
     q = rng.integers(2 ** 30, 2 ** 31, (4, 2000), dtype=np.uint64).astype(np.uint32)
     r = D.balance_microbatches(dev_u32(q), pl, 64, 2, 8, (1, 1))
     assert D.cand_result(r["best"])["status"] & D.DEV_MAKESPAN_OVERFLOW
+
+
+def test_split_pipeline_selected_for_config5(D, presets, monkeypatch):
+    """The bench workload runs the split pipeline by default (profile counts its chunks), and
+    DFLOP_SPLIT=0 turns it off -- with the same winner."""
+    monkeypatch.delenv("DFLOP_SPLIT", raising=False)
+    p = presets[5]
+    (t, f, x), (dt, df, dx) = feats(p, 0)
+    _, ticks = D.predict_costs(p.model, p.plan, dt, df, dx, want_f32=False)
+    K = 20000
+    D.profile_read(reset=True)
+    D.profile_enable(True)
+    a = D.cand_result(D.balance_microbatches(ticks, p.plan, K, p.R, p.G, p.seed(0))["best"])
+    pr = D.profile_read(reset=True)
+    monkeypatch.setenv("DFLOP_SPLIT", "0")
+    b = D.cand_result(D.balance_microbatches(ticks, p.plan, K, p.R, p.G, p.seed(0))["best"])
+    pr0 = D.profile_read(reset=True)
+    D.profile_enable(False)
+    assert pr["split_chunks"] >= 1 and pr0["split_chunks"] == 0
+    assert a == b
