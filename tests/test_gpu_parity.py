@@ -615,3 +615,21 @@ def test_split_pipeline_selected_for_config5(D, presets, monkeypatch):
     D.profile_enable(False)
     assert pr["split_chunks"] >= 1 and pr0["split_chunks"] == 0
     assert a == b
+
+
+def test_split_pipeline_order4(D, O, presets, monkeypatch):
+    """DFLOP_MODE_ORDER4 through the split pipeline (the ORDER4 instantiation of its candidate
+    kernel): every candidate of a 3,000-candidate family equals the merged kernel's, and a
+    window equals the oracle's ORDER4 mode."""
+    p = presets[5]
+    q = O.predict(p.model, p.plan, *p.features(3))[1]
+    qd = dev_u32(q)
+    K, seed = 3000, (5, 6)
+    monkeypatch.setenv("DFLOP_SPLIT", "0")
+    merged = gpu_balance(D, qd, p.plan, K, p.R, p.G, seed, 0, K, mode=16)
+    monkeypatch.setenv("DFLOP_SPLIT", "2")
+    monkeypatch.setenv("DFLOP_SPLIT_CHUNK", "1000")
+    split = gpu_balance(D, qd, p.plan, K, p.R, p.G, seed, 0, K, mode=16)
+    assert (split["cT"] == merged["cT"]).all() and (split["cC"] == merged["cC"]).all()
+    assert split["best"] == merged["best"] and (split["assign"] == merged["assign"]).all()
+    check_balance(D, O, q, p.plan, K, p.R, p.G, seed, 990, 1010, mode=16)
