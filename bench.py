@@ -431,6 +431,15 @@ def main():
         peak_alu = peak_issue / 2
         note = "fallback: 148 SM x 4 SMSP x 32 lanes x 1965 MHz (profiles/int_peaks.json missing)"
     variant = "u64" if wide_sums else "u32"
+    # the same work without the refinement pairs the windowed search proves irrelevant: on
+    # config 5 about 2% of the (i, i') pairs fall in a row's window (DESIGN.md section 6,
+    # oracle analysis of batch 0), so the refinement term shrinks to that share
+    frac_pruned = None
+    if not alg1 and prof.get("split_chunks"):
+        per = p.n / max(m, 1)
+        ref = 8.0 * p.R * per * (per + 1)
+        ops_pruned = (algorithmic_ops_per_candidate(p.n, m, S, p.R, p.G) - 0.98 * ref) * (e - b)
+        frac_pruned = ops_pruned / (cand_ms / 1e3) / 1e12
     kname = f"k_candidates<{variant}>"
     if variant == "u32" and prof.get("split_chunks"):  # the host launched the split pipeline
         kname = "k_lpt + k_candidates<u32> (split pipeline, %d chunks per step)" % (prof["split_chunks"] // args.steps)
@@ -441,7 +450,10 @@ def main():
                 "peak_note": note, "ops_per_candidate": ops_launch / max(1, (e - b) * P),
                 "ops_note": "nominal work of the method (DESIGN.md section 8); the split pipeline's windowed "
                             "refinement search scores only the pairs that could be applied (about 2% on config 5) "
-                            "with the same result -- ncu_* give the executed-instruction utilisation"}
+                            "with the same result -- frac_without_pruned_pairs counts only those, ncu_* give the "
+                            "executed-instruction utilisation"}
+    if frac_pruned is not None:
+        roofline["frac_without_pruned_pairs"] = frac_pruned / peak_issue
     stage_a = None
     if alg1:
         roofline["kernel"] = "k_candidates<u32> x P plans (Stage B, 4 streams)"
