@@ -676,7 +676,6 @@ dflop_status balance_launch(const BalanceArgs& a, const BalanceConfig& cfg, cons
             ql.lpt_el = reinterpret_cast<uint32_t*>(ws + cfg.o_lpt_el);
             q.lpt_apos = ql.lpt_apos;
             q.lpt_el = ql.lpt_el;
-            q.lpt_in = 1;
             const size_t ldyn = (size_t)cfg.lpt_tbl + (size_t)cfg.lpt_cpb * cfg.lpt_cb;
             cudaFuncSetAttribute(split_kernel_ptr(cfg.gl, p.order4 != 0),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.dyn);

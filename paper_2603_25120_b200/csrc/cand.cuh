@@ -49,11 +49,10 @@ struct CandParams {
     // split pipeline (packed variant): k_lpt runs the LPT of the candidates [c_begin, c_end)
     // and leaves, per candidate c, its assignment at lpt_apos + (c - c_begin) * apos_bytes and
     // its bucket loads (E, L packed keys, m x 2 u32) at lpt_el + (c - c_begin) * 2m; entry
-    // c_end - c_begin is a scratch entry for the tail groups; k_candidates with lpt_in = 1
-    // starts every candidate from there
+    // c_end - c_begin is a scratch entry for the tail groups; the candidate kernel's MODE = 1
+    // instantiation starts every candidate from there
     uint8_t* lpt_apos;
     uint32_t* lpt_el;
-    uint32_t lpt_in;
 };
 
 struct CandLaunch {

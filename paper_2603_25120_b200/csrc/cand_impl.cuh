@@ -1609,7 +1609,7 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
 // 16-byte stage in shared memory per candidate (≈0.5 KB instead of ≈2 KB), so ~300
 // candidates are resident per SM: the per-sample reduction and the two-sample bookkeeping
 // are shared by 4x more buckets per lane.  Writes each candidate's
-// assignment and final packed keys (offset removed) for k_candidates (lpt_in).
+// assignment and final packed keys (offset removed) for the candidate kernel (MODE = 1).
 template <int GL>
 __global__ void __launch_bounds__(kLptMaxThreads) k_lpt(CandParams p) {
     if (p.hdr->variant != 0) return;  // the packed variant only
