@@ -424,7 +424,7 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         lcb += 8;
     else
         while (lcb % 128 != 8u * (uint32_t)lg) lcb += 16;  // probe loads conflict-free (8-byte banks)
-    const uint32_t ltbl = (uint32_t)(((size_t)n * 16 + 127) & ~(size_t)127);
+    const uint32_t ltbl = (uint32_t)(((size_t)n * 8 + 127) & ~(size_t)127);  // (e, l) pairs only
     uint32_t lcpb = ltbl < smem_max ? (uint32_t)std::min<size_t>((smem_max - ltbl) / lcb, kLptMaxThreads / lg) : 0;
     lcpb = lcpb / lpw * lpw;
     const bool split_pre = sh.split_ok && split_env != 0 && !(sh.mode & DFLOP_MODE_EXHAUSTIVE) && m >= 48 &&

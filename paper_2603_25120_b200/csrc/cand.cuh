@@ -70,7 +70,10 @@ void cand_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 const void* split_kernel_ptr(int gl, bool o4);
 void split_launch(const CandLaunch& L, const CandParams& p, cudaStream_t s);
 // the split pipeline's LPT kernel (packed u32 variant, item table in shared memory)
-constexpr int kLptMaxThreads = 640;
+#ifndef DFLOP_LPT_MAX_THREADS
+#define DFLOP_LPT_MAX_THREADS 640
+#endif
+constexpr int kLptMaxThreads = DFLOP_LPT_MAX_THREADS;
 const void* lpt_kernel_ptr(int gl);
 void lpt_launch(int gl, uint32_t grid, uint32_t cpb, size_t dyn, const CandParams& p, cudaStream_t s);
 

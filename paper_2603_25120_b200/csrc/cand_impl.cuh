@@ -633,8 +633,8 @@ DFLOP_DEV void lpt_pair_step_q(Pair2<uint32_t>* EL, uint32_t pa, uint32_t pb, co
 // d = e' - l' + co >= 0: max(E' + d, L' + co) = max(E' + e', L' + l') - l' + co, the same
 // order over j (and the index bits) as the resulting max, without wrap-around (the variant's
 // bound covers probe + C); c == 0 probes with d = co.
-template <typename A, bool PK, int GL, bool SM>
-DFLOP_DEV void lpt_pass(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
+template <typename A, bool PK, int GL, bool SM, typename TB = Tbl<A, SM>>
+DFLOP_DEV void lpt_pass(const CandParams& p, const TB& T, uint32_t c, uint32_t sh, Pair2<A>* EL,
                         Pair2<A>* FL, uint8_t* apos, uint8_t* scr, uint32_t gl, uint32_t co, bool forced) {
     const uint32_t n = p.n, m = p.m, G = p.G;
     const bool wide = p.wide != 0;  // u16 assignment when m > 255
@@ -1604,6 +1604,17 @@ __global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
 }
 
 // ---------------------------------------------------------------- split pipeline: the LPT alone
+// k_lpt's item table: only the (e, l) half of every record, 8 bytes per sample (the LPT never
+// reads ef / lf), so the table takes half the shared memory
+struct TblEL {
+    uint32_t it_s;  // shared-window address of the (e, l) pairs
+    DFLOP_DEV Pair2<uint32_t> el(uint32_t pos) const {
+        Pair2<uint32_t> r;
+        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.a), "=r"(r.b) : "r"(it_s + pos * 8u));
+        return r;
+    }
+};
+
 // The LPT pass of the packed variant for the candidates [c_begin, c_end) with few lanes per
 // candidate (GL = m / 32: 32 buckets per lane for m = 64) and only the bucket keys and a
 // 16-byte stage in shared memory per candidate (≈0.5 KB instead of ≈2 KB), so ~300
@@ -1615,16 +1626,14 @@ __global__ void __launch_bounds__(kLptMaxThreads) k_lpt(CandParams p) {
     if (p.hdr->variant != 0) return;  // the packed variant only
     const uint32_t sh = p.hdr->shift, co = p.hdr->offs;
     extern __shared__ __align__(128) uint8_t smem[];
-    Tbl<uint32_t, true> T;
+    TblEL T;
     {
-        const uint32_t words = p.n * (uint32_t)sizeof(ItemRec<uint32_t>) / 16;
-        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x)
-            reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(p.items) + i);
+        for (uint32_t i = threadIdx.x; i < p.n; i += blockDim.x) {
+            const uint4 r = __ldg(reinterpret_cast<const uint4*>(p.items) + i);
+            reinterpret_cast<uint2*>(smem)[i] = make_uint2(r.x, r.y);
+        }
         __syncthreads();
-        T.it = reinterpret_cast<const ItemRec<uint32_t>*>(smem);
         T.it_s = (uint32_t)__cvta_generic_to_shared(smem);
-        T.pi16 = nullptr;
-        T.pi32 = nullptr;
     }
     bool forced = false;  // as in k_candidates
     if (p.m >= 1 && p.m <= p.n) {
@@ -1652,7 +1661,7 @@ __global__ void __launch_bounds__(kLptMaxThreads) k_lpt(CandParams p) {
         for (uint32_t j = gl; j < m; j += GL) EL[j] = Pair2<uint32_t>{j, j + co};
         for (uint32_t b = p.n + gl; b < p.apos_bytes; b += GL) apos[b] = 0xFF;  // padding: never a bucket
         __syncwarp(FULL);
-        lpt_pass<uint32_t, true, GL, true>(p, T, c, sh, EL, EL, apos, stage, gl, co, forced);
+        lpt_pass<uint32_t, true, GL, true, TblEL>(p, T, c, sh, EL, EL, apos, stage, gl, co, forced);
         Pair2<uint32_t>* dst = reinterpret_cast<Pair2<uint32_t>*>(p.lpt_el) + (size_t)e * m;
         for (uint32_t j = gl; j < m; j += GL) {
             const Pair2<uint32_t> x = EL[j];
