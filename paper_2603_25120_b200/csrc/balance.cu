@@ -440,14 +440,15 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     auto layout = [&](int v, uint32_t cap) {
         Lay L;
         uint32_t scr = round16(std::max((cfg.cnt_smem ? 8u * m + 4u : 0u) + 4u * cap, rings));
-        if (v == 0 && split_pre)  // the split kernel: rows' copy, then 64 sorted partner keys
-            scr = round16(std::max(round16(8u * m + 4u + 2u * cap) + 256u, rings));
+        if (v == 0 && split_pre)  // the split kernel: u32 counts, u16 offsets, rows' copy, 64 sorted keys
+            scr = round16(std::max(round16(4u * m + ((2u * m + 2u + 3u) & ~3u) + 2u * cap) + 256u, rings));
         const uint32_t asz = v == 2 ? 8u : 4u;
         const uint32_t el = round16(m * 2u * asz);   // EL[m] then FL[m]
         uint32_t cb = 2 * el + scr;
         // stagger consecutive candidates across banks: a group's probe touches GL*2*asz bytes
         uint32_t span = std::max(16u, (uint32_t)gl * 2u * asz);
         if (v == 0 && split_pre && stg_env >= 16 && stg_env < 128 && stg_env % 16 == 0) span = (uint32_t)stg_env;
+        if (v == 0 && split_pre && stg_env == 0) span = 128;  // no stagger
         if (span < 128) {
             const uint32_t want = span;  // a multiple of 16 below 128: reachable in <= 7 steps
             while (cb % 128 != want) cb += 16;
@@ -457,7 +458,8 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
         // stage the table in shared memory when it leaves room for at least 2 warps of candidates
         L.tbl_smem = (size_t)tbl + (size_t)2 * per_warp * cb <= smem_max;
         L.tbl = L.tbl_smem ? tbl : 0;
-        uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - L.tbl) / cb, kCandMaxThreads / gl);
+        const int max_threads = (v == 0 && split_pre) ? kSplitMaxThreads : kCandMaxThreads;
+        uint32_t cpb = (uint32_t)std::min<size_t>((smem_max - L.tbl) / cb, max_threads / gl);
         // no more groups than the family needs (one CTA per SM), whole warps only
         cpb = std::min<uint32_t>(cpb, std::max(1u, (sh.n_cand + nsm - 1) / nsm));
         if (forced_cpb >= (int)per_warp) cpb = std::min<uint32_t>(cpb, (uint32_t)forced_cpb);

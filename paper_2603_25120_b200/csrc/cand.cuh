@@ -16,6 +16,11 @@ constexpr int kVariants = 3;
 #define DFLOP_CAND_MAX_THREADS 640
 #endif
 constexpr int kCandMaxThreads = DFLOP_CAND_MAX_THREADS;
+// the split pipeline's candidate kernel (no LPT code; fewer registers)
+#ifndef DFLOP_SPLIT_MAX_THREADS
+#define DFLOP_SPLIT_MAX_THREADS 768
+#endif
+constexpr int kSplitMaxThreads = DFLOP_SPLIT_MAX_THREADS;
 
 // Per-launch parameters.  Shared-memory layout (bytes):
 //   [0, tbl_bytes)              CTA item table: ItemRec<A>[n] then u16 pos->item[n]

@@ -1,3 +1,4 @@
+#include <type_traits>
 // cand_impl.cuh -- the hot kernel of the path (a3 + a4): every candidate of the seeded
 // family (O6-O7) is one group of GL lanes of a warp:
 //
@@ -415,9 +416,9 @@ DFLOP_DEV void each_entry_rot(const uint4 v, uint32_t blk, uint32_t rot, uint32_
 // With FL != null (the first build after LPT) the count pass also forms the forward sums
 // FL[j] = (sum EF, sum LF) of the members (shared-memory atomics): the LPT steps then update
 // only EL -- one atomic per 8 entries of a warp instead of a read-modify-write per sample.
-template <typename A, int GL, bool SM>
+template <typename A, int GL, bool SM, typename OT = uint32_t>
 DFLOP_DEV void build_lists(const CandParams& p, const Tbl<A, SM>& T, const uint8_t* apos, bool wide, uint32_t* cnt,
-                           uint32_t* off, uint16_t* csr, uint32_t gl, Pair2<A>* FL) {
+                           OT* off, uint16_t* csr, uint32_t gl, Pair2<A>* FL) {
     const uint32_t m = p.m, nblk = p.apos_bytes / 16, sig = p.sigma;
     const uint4* ap = reinterpret_cast<const uint4*>(apos);
     for (uint32_t j = gl; j < m; j += GL) cnt[j] = 0;
@@ -453,12 +454,12 @@ DFLOP_DEV void build_lists(const CandParams& p, const Tbl<A, SM>& T, const uint8
             if (gl >= (uint32_t)d) inc += y;
         }
         if (j < m) {
-            off[j] = run + inc - v;
+            off[j] = (OT)(run + inc - v);
             cnt[j] = 0;
         }
         run += __shfl_sync(FULL, inc, GL - 1, GL);
     }
-    if (gl == 0) off[m] = run;
+    if (gl == 0) off[m] = (OT)run;
     __syncwarp(FULL);
     for (uint32_t b = gl; b < nblk; b += GL)
         each_entry(__ldcg(ap + b), b, wide, m, [&](uint32_t pos, uint32_t j) {
@@ -880,29 +881,37 @@ DFLOP_DEV void refine(const CandParams& p, const Tbl<A, SM>& T, uint32_t c, uint
     // cnt[m] members per bucket, off[m + 1] list starts: in shared memory (m <= 256), else
     // in front of the slot's global lists; then the shared-memory copies of the first cap
     // members of j* (ls) and j' (lp)
+    // the split kernel (CS) keeps the list offsets as u16 (n + m * sigma < 65536 there)
+    using OT = std::conditional_t<CS, uint16_t, uint32_t>;
     uint32_t* cnt;
     uint16_t* ls;
-    if (CS || p.cnt_smem) {
+    OT* off;
+    if (CS) {
         cnt = reinterpret_cast<uint32_t*>(scr);
+        off = reinterpret_cast<OT*>(cnt + m);
+        ls = reinterpret_cast<uint16_t*>(scr + 4u * m + ((2u * m + 2u + 3u) & ~3u));
+    } else if (p.cnt_smem) {
+        cnt = reinterpret_cast<uint32_t*>(scr);
+        off = reinterpret_cast<OT*>(cnt + m);
         ls = reinterpret_cast<uint16_t*>(cnt + 2 * m + 1);
     } else {
         cnt = reinterpret_cast<uint32_t*>(csr);
+        off = reinterpret_cast<OT*>(cnt + m);
         csr += 2 * (2 * m + 1);
         ls = reinterpret_cast<uint16_t*>(scr);
     }
-    uint32_t* off = cnt + m;
     uint16_t* lp = ls + cap;
     // SRT (split kernel, 32-bit sums, table in shared memory, n <= 4096): j''s members are
     // sorted by their load in the narrower of the two dimensions and each row scans only the
     // window of partners that could bring the pair below W* (DESIGN.md section 6); the sorted
     // keys (load with the low 12 bits replaced by the position) follow the row copy
     constexpr bool SRT = CS && SM && sizeof(A) == 4 && GL >= 8;
-    uint32_t* sk = reinterpret_cast<uint32_t*>(scr + ((4u * (2u * m + 1u) + 2u * cap + 15u) & ~15u));
+    uint32_t* sk = reinterpret_cast<uint32_t*>(scr + ((4u * m + ((2u * m + 2u + 3u) & ~3u) + 2u * cap + 15u) & ~15u));
     bool dirty = true;  // the lists must be (re)built from the assignment
     bool first = true;  // the first build also forms FL (LPT maintains EL only)
     for (uint32_t r = 0; r < p.R; ++r) {
         if (__any_sync(FULL, dirty)) {  // warp-uniform: a clean group rebuilds the same lists
-            build_lists<A, GL, SM>(p, T, apos, wide, cnt, off, csr, gl, first ? FL : nullptr);
+            build_lists<A, GL, SM, OT>(p, T, apos, wide, cnt, off, csr, gl, first ? FL : nullptr);
             dirty = false;
             first = false;
         }
@@ -1476,7 +1485,7 @@ DFLOP_DEV void run_candidate(const CandParams& p, const Tbl<A, SM>& T, uint32_t 
 // MODE 0: the whole candidate (LPT, refinement, 1F1B); 1: the split pipeline's second kernel
 // (from k_lpt's output: refinement + 1F1B; packed u32 only)
 template <typename A, bool PK, int GL, bool SM, bool O4, int MODE = 0>
-__global__ void __launch_bounds__(kCandMaxThreads) k_candidates(CandParams p) {
+__global__ void __launch_bounds__(MODE != 0 ? kSplitMaxThreads : kCandMaxThreads) k_candidates(CandParams p) {
     if (p.hdr->variant != p.want_variant) return;  // another variant runs
     uint32_t sh = PK ? p.hdr->shift : 0u;
     uint32_t co = PK ? p.hdr->offs : 0u;  // LPT probe offset (lpt_pass)
