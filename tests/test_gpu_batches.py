@@ -98,3 +98,22 @@ def test_batch_offset_errors(D, presets):
     t, f, x = (dev_u32(a) for a in p.features(0))
     with pytest.raises(Exception, match="offsets"):
         D.search_plans_batches(p.model, t, f, x, [0, 100, 50], K=8, R=1, G=8, seed=(1, 2), plan=p.plan)
+
+
+def test_split_pipeline_over_ragged_batches(D, presets, monkeypatch):
+    """Config 5's shape over three ragged batches (4,096 / 3,000 / 1,500 samples) at K = 6,000:
+    the split pipeline (each batch's own workspace need within the bound computed for the
+    largest; a batch whose chunks would outgrow it falls back to the merged kernel) gives the
+    merged kernel's per-batch winners and assignments."""
+    p = presets[5]
+    feats, offs, cat = sample(p, [0, 1, 2], [4096, 3000, 1500])
+    t, f, x = (dev_u32(a) for a in cat)
+    K = 6000
+    monkeypatch.delenv("DFLOP_SPLIT", raising=False)
+    a = D.search_plans_batches(p.model, t, f, x, offs, K=K, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan)
+    monkeypatch.setenv("DFLOP_SPLIT", "0")
+    b = D.search_plans_batches(p.model, t, f, x, offs, K=K, R=p.R, G=p.G, seed=p.seed(0), plan=p.plan)
+    assert a["makespan"] == b["makespan"]
+    for ga, gb in zip(a["batches"], b["batches"]):
+        assert ga["makespan"] == gb["makespan"] and ga["cand"] == gb["cand"] and ga["cmax"] == gb["cmax"]
+    assert (host_u32(a["assign"]) == host_u32(b["assign"])).all()
