@@ -398,7 +398,12 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     // CSR member lists of the refinement: every bucket gets its LPT
     // count plus sigma free entries (a move adds one member to j'); a list that would
     // overflow triggers a rebuild from the assignment
-    cfg.sigma = std::max(1u, std::min(std::max(1u, sh.R), per_bucket));
+    // two free entries per list: a bucket gaining a third member in one candidate is rare and
+    // only triggers a rebuild, while the smaller lists keep more of the slots' scratch in the
+    // L2 (config 5: sigma 16 -> 2, -1%; configs 2/3: -2..-4%)
+    cfg.sigma = std::max(1u, std::min(2u, std::min(std::max(1u, sh.R), per_bucket)));
+    const int fsig = env_int("DFLOP_SIGMA", 0);  // experiments: free list entries per bucket
+    if (fsig >= 1 && fsig <= 256) cfg.sigma = (uint32_t)fsig;
     // counters cnt[m] and offsets off[m + 1] (u32) in shared memory up to m = 256, else in
     // front of the slot's global lists
     cfg.cnt_smem = m <= 256;
