@@ -519,19 +519,12 @@ BalanceConfig balance_config(const BalanceShape& sh, int device) {
     cfg.n_slots = 0;
     for (int v = 0; v < 3; ++v) cfg.n_slots = std::max(cfg.n_slots, cfg.grid[v] * cfg.cpb[v]);
     if (split_pre && cfg.tbl_smem[0] && cfg.cpb[0] > 0) {
-        // chunks of r LPT rounds, r chosen so that the candidate kernel's rounds over a chunk
-        // are nearly whole
-        const uint32_t wave = nsm * lcpb, res0 = cfg.grid[0] * cfg.cpb[0];
-        uint32_t best_r = 4;
-        double best_w = 1e9;
-        for (uint32_t r = 3; r <= 8; ++r) {
-            const double rounds = (double)wave * r / res0;
-            const double w = (std::ceil(rounds) - rounds) / std::ceil(rounds);
-            if (w < best_w - 1e-9) {
-                best_w = w;
-                best_r = r;
-            }
-        }
+        // chunks of r whole k_lpt waves, as few as the entry buffer allows: every chunk boundary
+        // costs a partly filled k_lpt wave and candidate-kernel round (config 5: 10^6 candidates
+        // in one chunk 94.5 ms, in chunks of 6 waves 97.4 ms); the entries take ~4.6 KB per
+        // candidate, so a chunk is capped at 2^20 candidates (~4.8 GB)
+        const uint32_t wave = nsm * lcpb;
+        uint32_t best_r = std::max(1u, (1u << 20) / std::max(1u, wave));
         const int fr = env_int("DFLOP_SPLIT_ROUNDS", 0);
         if (fr >= 1 && fr <= 64) best_r = (uint32_t)fr;
         cfg.split = true;
