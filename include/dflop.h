@@ -273,7 +273,11 @@ dflop_status dflop_predict_costs(const dflop_cost_model* model, const dflop_plan
  *   plan           host; only e_pp, l_pp, l_dp, n_mb are used.
  *   ws / ws_bytes  workspace query: ws == NULL stores the required size in *ws_bytes
  *                  and returns OK without launching; otherwise ws must be a device
- *                  buffer of at least *ws_bytes bytes, 256-byte aligned.
+ *                  buffer of at least *ws_bytes bytes, 256-byte aligned.  It holds the
+ *                  per-resident-candidate scratch (about 18 KB each for n = 4096, m = 64)
+ *                  and, when the split pipeline runs (packed sums,
+ *                  48 <= m <= 255, n <= 4096, >= 4,096 candidates), one entry of n + 8m
+ *                  bytes per candidate of the range, up to 2^20 candidates per chunk.
  *   best           device dflop_cand_result (written).
  *   assign         device u32[n] or NULL: bucket of every sample for c*.
  *   group_offsets  device u32[m+1] or NULL, group_items device u32[n] or NULL: the
