@@ -170,6 +170,21 @@ DFLOP_DEV uint64_t batch_perms(uint32_t g0, uint32_t W, uint32_t nc, uint32_t c,
         uint64_t perm = 0xFEDCBA9876543210ull;
         uint32_t p32 = 0x76543210u;
         const bool narrow = G <= 8;
+        if (ng == 8u && nc == 2u) {  // a full group of 8 (every preset): 7 steps, no bounds tests
+            const Philox4 r0 = philox4x32_10(g0 + gg, cc, 0u, 0u, k0, k1);
+            const Philox4 r1 = philox4x32_10(g0 + gg, cc, 0u, 1u, k0, k1);
+            const uint32_t wq[7] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z};
+#pragma unroll
+            for (uint32_t idx = 0; idx < 7; ++idx) {
+                const uint32_t tt = 7 - idx;
+                const uint32_t rr = mulhi32(wq[idx], tt + 1);
+                const uint32_t x = ((p32 >> (4 * tt)) ^ (p32 >> (4 * rr))) & 15u;
+                p32 ^= (x << (4 * tt)) | (x << (4 * rr));
+            }
+            perm = 0xFEDCBA9800000000ull | p32;
+            if (cc < 2) perm = 0xFEDCBA9876543210ull;
+            return perm;
+        }
         for (uint32_t pc = 0; pc < nc; ++pc) {
             const Philox4 r = philox4x32_10(g0 + gg, cc, 0u, pc, k0, k1);
             const uint32_t wq[4] = {r.x, r.y, r.z, r.w};
