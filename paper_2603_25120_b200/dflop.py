@@ -333,6 +333,20 @@ class Workspace:
 _default_ws = Workspace()
 
 
+def balance_workspace_bytes(n: int, plan: Dict, K: int, R: int, G: int, c_begin: int = 0,
+                            c_end: Optional[int] = None, mode: int = MODE_HEURISTIC) -> int:
+    """The workspace dflop_balance_microbatches needs for this shape (its ws == NULL query)."""
+    c_end = K if c_end is None else c_end
+    bp = BalanceParams()
+    bp.struct_size = C.sizeof(BalanceParams)
+    bp.mode, bp.K, bp.cand_begin, bp.cand_end, bp.R, bp.G = mode, K, c_begin, c_end, R, G
+    ps = plan_struct(plan)
+    need = C.c_size_t(0)
+    _check(lib().dflop_balance_microbatches(None, n, C.byref(ps), C.byref(bp), None, C.byref(need), None,
+                                            None, None, None, None, None, None))
+    return int(need.value)
+
+
 def balance_microbatches(cost_ticks, plan: Dict, K: int, R: int, G: int, seed: Sequence[int], c_begin: int = 0,
                          c_end: Optional[int] = None, mode: int = MODE_HEURISTIC, id_base: int = 0,
                          want_assign: bool = True, want_groups: bool = False, per_candidate: bool = False,

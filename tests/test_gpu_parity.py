@@ -633,3 +633,15 @@ def test_split_pipeline_order4(D, O, presets, monkeypatch):
     assert (split["cT"] == merged["cT"]).all() and (split["cC"] == merged["cC"]).all()
     assert split["best"] == merged["best"] and (split["assign"] == merged["assign"]).all()
     check_balance(D, O, q, p.plan, K, p.R, p.G, seed, 990, 1010, mode=16)
+
+
+def test_split_pipeline_workspace_bound(D, presets):
+    """The split pipeline's entries (n + 8m bytes per candidate) are sized for the chunk, which
+    is capped at 2^20 candidates: config 5 at K = 10^6 holds them all, at K = 2^22 the chunk
+    (and the workspace) stops growing."""
+    p = presets[5]
+    entry = p.n + 8 * p.plan["n_mb"] * p.plan["l_dp"]
+    w1 = D.balance_workspace_bytes(p.n, p.plan, 10 ** 6, p.R, p.G)
+    w4 = D.balance_workspace_bytes(p.n, p.plan, 1 << 22, p.R, p.G)
+    assert w1 >= 10 ** 6 * entry
+    assert w4 <= (1 << 20) * entry + (w1 - 10 ** 6 * entry) + (1 << 26)
